@@ -1,0 +1,741 @@
+/*
+ * mhd_oracle.c — TEST INFRASTRUCTURE ONLY (see mhd_oracle.h).
+ *
+ * The plain CPU oracle of the fp64 ideal-MHD Godunov step of arxiv 2510.24175
+ * (gPLUTO's 5-step RK pipeline, §3.2; double precision,
+ * PAPER.md:179 §4.2; GLM divergence cleaning).
+ *
+ * The paper gives no formulas.  This file follows, step by step and in the
+ * same order and association, the recipe written in DESIGN.md §3
+ * ("Readings"), which restates SURVEY.md §8(c) c.0-c.17:
+ *   c.2 ghost fill, c.3 cons->prim, c.4 face prim->cons + fast speed,
+ *   c.5 PLM (minmod / MC), c.6 GLM interface pre-solve, c.7 physical flux,
+ *   c.8 HLL (Miyoshi-Kusano eq. 67 speed bounds), c.9 HLLD (Miyoshi & Kusano
+ *   2005), c.10 flux assembly, c.11 stage operator + RK2, c.12 GLM damping,
+ *   c.13 CFL dt and c_h.
+ * Arithmetic discipline (c.0 / DESIGN.md R-ARITH): compiled with
+ * -ffp-contract=off and without -ffast-math; only + - * / sqrt fabs fmin fmax
+ * per cell; every expression is evaluated exactly as parenthesised here.
+ *
+ * No blocking, fusion or reordering: each stage materialises the padded
+ * state, the primitive array, the PLM face states and the face fluxes of
+ * every direction, then applies the update.  OpenMP only splits the outer
+ * loop of each pass; every output element is written by exactly one
+ * iteration and the only reductions are integer sums and exact max/min, so
+ * results are bitwise independent of the thread count.
+ */
+#include "mhd_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_E_ARG 1
+#define ORC_E_UNPHYSICAL 6
+
+/* ------------------------------------------------------------------------ */
+/* grid bookkeeping                                                          */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t n[3];   /* interior cells */
+  int64_t g[3];   /* ghost width: 2 on active axes (PLM, c.1), 0 otherwise */
+  int64_t m[3];   /* padded extent n + 2g */
+  int act[3];     /* axis active (R7) */
+  int nvar;       /* 8 + glm */
+  double dx[3];   /* (hi-lo)/n, host double (c.1) */
+} grid_t;
+
+static int make_grid(const orc_config* c, grid_t* G) {
+  if (!c) return ORC_E_ARG;
+  if (!(c->gamma > 1.0) || !(c->cfl > 0.0 && c->cfl < 1.0)) return ORC_E_ARG;
+  int nact = 0;
+  for (int d = 0; d < 3; ++d) {
+    if (c->n[d] < 1) return ORC_E_ARG;
+    G->n[d] = c->n[d];
+    G->act[d] = c->n[d] > 1;
+    if (G->act[d] && c->n[d] < 4) return ORC_E_ARG;
+    G->g[d] = G->act[d] ? 2 : 0;
+    G->m[d] = G->n[d] + 2 * G->g[d];
+    if (!(c->hi[d] > c->lo[d])) return ORC_E_ARG;
+    G->dx[d] = (c->hi[d] - c->lo[d]) / (double)c->n[d];
+    nact += G->act[d];
+  }
+  if (nact == 0) return ORC_E_ARG;
+  G->nvar = 8 + (c->glm ? 1 : 0);
+  return ORC_OK;
+}
+
+/* index of field f at interior coordinates (i,j,k); ghosts are negative or >= n */
+static inline size_t P(const grid_t* G, int f, int64_t i, int64_t j, int64_t k) {
+  return (((size_t)f * G->m[2] + (size_t)(k + G->g[2])) * G->m[1] + (size_t)(j + G->g[1])) * G->m[0] +
+         (size_t)(i + G->g[0]);
+}
+static inline size_t padded_size(const grid_t* G) { return (size_t)G->nvar * G->m[0] * G->m[1] * G->m[2]; }
+static inline int64_t interior_linear(const grid_t* G, int64_t i, int64_t j, int64_t k) {
+  return (k * G->n[1] + j) * G->n[0] + i;
+}
+
+/* copy interior U[f][z][y][x] <-> padded */
+static void load_interior(const grid_t* G, const double* U, double* Up) {
+  for (int f = 0; f < G->nvar; ++f)
+    for (int64_t k = 0; k < G->n[2]; ++k)
+      for (int64_t j = 0; j < G->n[1]; ++j)
+        for (int64_t i = 0; i < G->n[0]; ++i)
+          Up[P(G, f, i, j, k)] = U[(((size_t)f * G->n[2] + k) * G->n[1] + j) * G->n[0] + i];
+}
+static void store_interior(const grid_t* G, const double* Up, double* U) {
+  for (int f = 0; f < G->nvar; ++f)
+    for (int64_t k = 0; k < G->n[2]; ++k)
+      for (int64_t j = 0; j < G->n[1]; ++j)
+        for (int64_t i = 0; i < G->n[0]; ++i)
+          U[(((size_t)f * G->n[2] + k) * G->n[1] + j) * G->n[0] + i] = Up[P(G, f, i, j, k)];
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.2 ghost fill (row a1): periodic wrap or zero-gradient outflow, 2 cells   */
+/* ------------------------------------------------------------------------ */
+static void fill_ghosts(const orc_config* c, const grid_t* G, double* Up) {
+  for (int d = 0; d < 3; ++d) {
+    if (!G->act[d]) continue;
+    const int64_t N = G->n[d];
+    /* the two other axes, interior range (edge/corner ghosts are never read) */
+    const int a = (d + 1) % 3, b = (d + 2) % 3;
+    for (int f = 0; f < G->nvar; ++f)
+      for (int64_t q = 0; q < G->n[b]; ++q)
+        for (int64_t r = 0; r < G->n[a]; ++r) {
+          int64_t idx[3];
+          idx[a] = r;
+          idx[b] = q;
+#define AT(s) (*(idx[d] = (s), &Up[P(G, f, idx[0], idx[1], idx[2])]))
+          if (c->bc_lo[d] == 0) { /* periodic: U[-1]=U[N-1], U[-2]=U[N-2] */
+            double v1 = AT(N - 1), v2 = AT(N - 2);
+            AT(-1) = v1;
+            AT(-2) = v2;
+          } else { /* outflow: U[-2]=U[-1]=U[0] */
+            double v0 = AT(0);
+            AT(-1) = v0;
+            AT(-2) = v0;
+          }
+          if (c->bc_hi[d] == 0) { /* periodic: U[N]=U[0], U[N+1]=U[1] */
+            double v0 = AT(0), v1 = AT(1);
+            AT(N) = v0;
+            AT(N + 1) = v1;
+          } else { /* outflow: U[N]=U[N+1]=U[N-1] */
+            double vl = AT(N - 1);
+            AT(N) = vl;
+            AT(N + 1) = vl;
+          }
+#undef AT
+        }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.3 conservative -> primitive (row a2)                                     */
+/* ------------------------------------------------------------------------ */
+int orc_cons2prim(const orc_config* c, const double* U, double* V) {
+  const double gm1 = c->gamma - 1.0;
+  const double rho = U[0], mx = U[1], my = U[2], mz = U[3], E = U[4];
+  const double Bx = U[5], By = U[6], Bz = U[7];
+  const double ir = 1.0 / rho;
+  const double vx = mx * ir, vy = my * ir, vz = mz * ir;
+  const double ke = 0.5 * ((mx * vx + my * vy) + mz * vz);
+  const double me = 0.5 * ((Bx * Bx + By * By) + Bz * Bz);
+  double p = gm1 * ((E - ke) - me);
+  int floored = 0;
+  if (p < c->p_floor) {
+    p = c->p_floor;
+    floored = 1;
+  }
+  V[0] = rho;
+  V[1] = vx;
+  V[2] = vy;
+  V[3] = vz;
+  V[4] = p;
+  V[5] = Bx;
+  V[6] = By;
+  V[7] = Bz;
+  if (c->glm) V[8] = U[8]; /* psi passes through */
+  return floored;
+}
+
+static int bad_cell(const double* U, int nvar) {
+  if (!(U[0] > 0.0)) return 1;
+  for (int f = 0; f < nvar; ++f)
+    if (!isfinite(U[f])) return 1;
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.4 face-state energy and fast magnetosonic speed                          */
+/* ------------------------------------------------------------------------ */
+double orc_total_energy(double gamma, const double* V) {
+  /* E = (p/(gamma-1) + 0.5 rho |v|^2) + 0.5 |B|^2, associated as c.4 */
+  const double igm1 = 1.0 / (gamma - 1.0);
+  const double kin2 = (V[1] * V[1] + V[2] * V[2]) + V[3] * V[3];
+  const double bt_sq = V[6] * V[6] + V[7] * V[7];
+  const double mag2 = V[5] * V[5] + bt_sq;
+  return (V[4] * igm1 + (0.5 * V[0]) * kin2) + 0.5 * mag2;
+}
+
+double orc_fast_speed(double gamma, double rho, double p, double bn, double bt1, double bt2) {
+  const double bt_sq = bt1 * bt1 + bt2 * bt2;
+  const double ir = 1.0 / rho;
+  const double a2 = (gamma * p) * ir;
+  const double bn2 = (bn * bn) * ir;
+  const double bt2n = bt_sq * ir;
+  const double b2 = bn2 + bt2n;
+  const double dd = (a2 - b2) * (a2 - b2) + (4.0 * a2) * bt2n; /* (a2+b2)^2 - 4 a2 bn2, never negative */
+  return sqrt(0.5 * ((a2 + b2) + sqrt(dd)));
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.5 limiters                                                               */
+/* ------------------------------------------------------------------------ */
+double orc_limited_slope(int32_t limiter, double dm, double dp) {
+  if (limiter == 0) { /* minmod */
+    if (dm > 0.0 && dp > 0.0) return fmin(dm, dp);
+    if (dm < 0.0 && dp < 0.0) return fmax(dm, dp);
+    return 0.0;
+  }
+  /* monotonised central (van Leer 1977) */
+  const double cc = 0.5 * (dm + dp);
+  if (dm > 0.0 && dp > 0.0) return fmin(fmin(2.0 * dm, 2.0 * dp), cc);
+  if (dm < 0.0 && dp < 0.0) return fmax(fmax(2.0 * dm, 2.0 * dp), cc);
+  return 0.0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.6-c.10 face flux in the normal frame                                     */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  double rho, vn, vt1, vt2, p, bn, bt1, bt2;
+  double E, pt, cf;
+  double U[8]; /* (rho, mn, mt1, mt2, E, Bn, Bt1, Bt2) */
+  double F[8]; /* physical flux, c.7 */
+} side_t;
+
+/* c.4 + c.7 for one side; bn already replaced by Bm (c.6) */
+static void side_state(double gamma, double igm1, const double* V, double bn, side_t* s) {
+  s->rho = V[0];
+  s->vn = V[1];
+  s->vt1 = V[2];
+  s->vt2 = V[3];
+  s->p = V[4];
+  s->bn = bn;
+  s->bt1 = V[6];
+  s->bt2 = V[7];
+  /* c.4 */
+  const double kin2 = (s->vn * s->vn + s->vt1 * s->vt1) + s->vt2 * s->vt2;
+  const double bt_sq = s->bt1 * s->bt1 + s->bt2 * s->bt2;
+  const double mag2 = s->bn * s->bn + bt_sq;
+  s->E = (s->p * igm1 + (0.5 * s->rho) * kin2) + 0.5 * mag2;
+  const double mn = s->rho * s->vn, mt1 = s->rho * s->vt1, mt2 = s->rho * s->vt2;
+  s->pt = s->p + 0.5 * mag2;
+  const double ir = 1.0 / s->rho;
+  const double a2 = (gamma * s->p) * ir;
+  const double bn2 = (s->bn * s->bn) * ir;
+  const double bt2 = bt_sq * ir;
+  const double b2 = bn2 + bt2;
+  const double dd = (a2 - b2) * (a2 - b2) + (4.0 * a2) * bt2;
+  s->cf = sqrt(0.5 * ((a2 + b2) + sqrt(dd)));
+  s->U[0] = s->rho;
+  s->U[1] = mn;
+  s->U[2] = mt1;
+  s->U[3] = mt2;
+  s->U[4] = s->E;
+  s->U[5] = s->bn;
+  s->U[6] = s->bt1;
+  s->U[7] = s->bt2;
+  /* c.7 */
+  const double fm = s->rho * s->vn;
+  s->F[0] = fm;
+  s->F[1] = (fm * s->vn + s->pt) - s->bn * s->bn;
+  s->F[2] = fm * s->vt1 - s->bn * s->bt1;
+  s->F[3] = fm * s->vt2 - s->bn * s->bt2;
+  const double vB = (s->vn * s->bn + s->vt1 * s->bt1) + s->vt2 * s->bt2;
+  s->F[4] = (s->E + s->pt) * s->vn - s->bn * vB;
+  s->F[5] = 0.0;
+  s->F[6] = s->bt1 * s->vn - s->bn * s->vt1;
+  s->F[7] = s->bt2 * s->vn - s->bn * s->vt2;
+}
+
+/* c.8 HLL average of the 8 MHD components */
+static void hll_flux(const side_t* L, const side_t* R, double SL, double SR, double* F) {
+  const double isd = 1.0 / (SR - SL);
+  for (int k = 0; k < 8; ++k) F[k] = ((SR * L->F[k] - SL * R->F[k]) + (SL * SR) * (R->U[k] - L->U[k])) * isd;
+}
+
+/* c.9 star state of one side (Miyoshi & Kusano 2005 eqs. 43-48) */
+typedef struct {
+  double sd, m, sm, rhos, vst1, vst2, bst1, bst2, vBs, Es;
+  double Us[8];
+} star_t;
+
+static void star_state(const side_t* s, double S, double SM, double pts, double B, star_t* t) {
+  t->sd = S - s->vn;
+  t->m = s->rho * t->sd;
+  t->sm = S - SM;
+  t->rhos = t->m / t->sm;
+  const double d = t->m * t->sm - B * B;
+  if (fabs(d) < 1e-8 * pts) { /* degenerate (R6): no tangential jump */
+    t->vst1 = s->vt1;
+    t->vst2 = s->vt2;
+    t->bst1 = s->bt1;
+    t->bst2 = s->bt2;
+  } else {
+    const double id = 1.0 / d;
+    const double cv = (B * (SM - s->vn)) * id;
+    const double cb = (t->m * t->sd - B * B) * id;
+    t->vst1 = s->vt1 - s->bt1 * cv;
+    t->vst2 = s->vt2 - s->bt2 * cv;
+    t->bst1 = s->bt1 * cb;
+    t->bst2 = s->bt2 * cb;
+  }
+  const double vB = (s->vn * B + s->vt1 * s->bt1) + s->vt2 * s->bt2;
+  t->vBs = (SM * B + t->vst1 * t->bst1) + t->vst2 * t->bst2;
+  t->Es = (((t->sd * s->E - s->pt * s->vn) + pts * SM) + B * (vB - t->vBs)) / t->sm;
+  t->Us[0] = t->rhos;
+  t->Us[1] = t->rhos * SM;
+  t->Us[2] = t->rhos * t->vst1;
+  t->Us[3] = t->rhos * t->vst2;
+  t->Us[4] = t->Es;
+  t->Us[5] = B;
+  t->Us[6] = t->bst1;
+  t->Us[7] = t->bst2;
+}
+
+int orc_face_flux(const orc_config* c, const double* VLin, const double* VRin, double ch, double* F) {
+  const double gamma = c->gamma;
+  const double igm1 = 1.0 / (gamma - 1.0);
+  /* c.6 GLM interface pre-solve (Dedner 2002 eq. 41 as used by Mignone & Tzeferacos 2010) */
+  double Bm, psim = 0.0;
+  if (c->glm) {
+    const double hc = 0.5 * ch, ihc = 0.5 / ch;
+    Bm = 0.5 * (VLin[5] + VRin[5]) - ihc * (VRin[8] - VLin[8]);
+    psim = 0.5 * (VLin[8] + VRin[8]) - hc * (VRin[5] - VLin[5]);
+  } else {
+    Bm = 0.5 * (VLin[5] + VRin[5]);
+  }
+  side_t L, R;
+  side_state(gamma, igm1, VLin, Bm, &L);
+  side_state(gamma, igm1, VRin, Bm, &R);
+
+  /* c.8 signal speeds (Miyoshi & Kusano 2005 eq. 67) */
+  const double cmax = fmax(L.cf, R.cf);
+  const double SL = fmin(L.vn, R.vn) - cmax;
+  const double SR = fmax(L.vn, R.vn) + cmax;
+  double Fm[8];
+  int fell_back = 0;
+  if (SL > 0.0) {
+    memcpy(Fm, L.F, sizeof Fm);
+  } else if (SR < 0.0) {
+    memcpy(Fm, R.F, sizeof Fm);
+  } else if (c->riemann == 0) {
+    hll_flux(&L, &R, SL, SR, Fm);
+  } else {
+    /* c.9 HLLD */
+    const double B = Bm;
+    const double sdL = SL - L.vn, sdR = SR - R.vn;
+    const double mL = L.rho * sdL, mR = R.rho * sdR;
+    const double iden = 1.0 / (mR - mL);
+    const double SM = (((mR * R.vn - mL * L.vn) - R.pt) + L.pt) * iden;               /* eq. 38 */
+    const double pts = ((mR * L.pt - mL * R.pt) + (mL * mR) * (R.vn - L.vn)) * iden;  /* eq. 41 */
+    if (!(SL < SM && SM < SR)) {
+      hll_flux(&L, &R, SL, SR, Fm);
+      fell_back = 1;
+    } else {
+      star_t sL, sR;
+      star_state(&L, SL, SM, pts, B, &sL);
+      star_state(&R, SR, SM, pts, B, &sR);
+      const double srL = sqrt(sL.rhos), srR = sqrt(sR.rhos);
+      const double SsL = SM - fabs(B) / srL; /* eq. 51 */
+      const double SsR = SM + fabs(B) / srR;
+      if (!(SL <= SsL && SsR <= SR)) { /* wave-ordering guard (R7) */
+        hll_flux(&L, &R, SL, SR, Fm);
+        fell_back = 1;
+      } else {
+        double FsL[8], FsR[8];
+        for (int k = 0; k < 8; ++k) FsL[k] = L.F[k] + SL * (sL.Us[k] - L.U[k]); /* eq. 64 */
+        for (int k = 0; k < 8; ++k) FsR[k] = R.F[k] + SR * (sR.Us[k] - R.U[k]);
+        if (SsL >= 0.0) {
+          memcpy(Fm, FsL, sizeof Fm);
+        } else if (SM >= 0.0 || SsR >= 0.0) {
+          /* double-star states, eqs. 59-63 */
+          const double sg = (B >= 0.0) ? 1.0 : -1.0;
+          const double is = 1.0 / (srL + srR);
+          const double vss1 = ((srL * sL.vst1 + srR * sR.vst1) + (sR.bst1 - sL.bst1) * sg) * is;
+          const double vss2 = ((srL * sL.vst2 + srR * sR.vst2) + (sR.bst2 - sL.bst2) * sg) * is;
+          const double bss1 = ((srL * sR.bst1 + srR * sL.bst1) + ((srL * srR) * (sR.vst1 - sL.vst1)) * sg) * is;
+          const double bss2 = ((srL * sR.bst2 + srR * sL.bst2) + ((srL * srR) * (sR.vst2 - sL.vst2)) * sg) * is;
+          const double vBss = (SM * B + vss1 * bss1) + vss2 * bss2;
+          if (SM >= 0.0) {
+            const double EssL = sL.Es - (srL * (sL.vBs - vBss)) * sg;
+            const double Uss[8] = {sL.rhos, sL.rhos * SM, sL.rhos * vss1, sL.rhos * vss2, EssL, B, bss1, bss2};
+            for (int k = 0; k < 8; ++k) Fm[k] = FsL[k] + SsL * (Uss[k] - sL.Us[k]); /* eq. 65 */
+          } else {
+            const double EssR = sR.Es + (srR * (sR.vBs - vBss)) * sg;
+            const double Uss[8] = {sR.rhos, sR.rhos * SM, sR.rhos * vss1, sR.rhos * vss2, EssR, B, bss1, bss2};
+            for (int k = 0; k < 8; ++k) Fm[k] = FsR[k] + SsR * (Uss[k] - sR.Us[k]);
+          }
+        } else {
+          memcpy(Fm, FsR, sizeof Fm);
+        }
+      }
+    }
+  }
+  /* c.10 assembly */
+  for (int k = 0; k < 8; ++k) F[k] = Fm[k];
+  if (c->glm) {
+    F[5] = psim;
+    F[8] = (ch * ch) * Bm;
+  } else {
+    F[5] = 0.0;
+  }
+  return fell_back;
+}
+
+int64_t orc_face_flux_batch(const orc_config* c, const double* VL, const double* VR, int64_t n, double ch,
+                            double* F) {
+  const int nvar = 8 + (c->glm ? 1 : 0);
+  int64_t fb = 0;
+  for (int64_t q = 0; q < n; ++q) fb += orc_face_flux(c, VL + q * nvar, VR + q * nvar, ch, F + q * nvar);
+  return fb;
+}
+
+/* ------------------------------------------------------------------------ */
+/* frame permutation (R8): x:(x,y,z), y:(y,z,x), z:(z,x,y)                    */
+/* ------------------------------------------------------------------------ */
+static void to_normal(int d, int nvar, const double* V, double* W) {
+  const int n = d, t1 = (d + 1) % 3, t2 = (d + 2) % 3;
+  W[0] = V[0];
+  W[1] = V[1 + n];
+  W[2] = V[1 + t1];
+  W[3] = V[1 + t2];
+  W[4] = V[4];
+  W[5] = V[5 + n];
+  W[6] = V[5 + t1];
+  W[7] = V[5 + t2];
+  if (nvar > 8) W[8] = V[8];
+}
+static void from_normal(int d, int nvar, const double* W, double* V) {
+  const int n = d, t1 = (d + 1) % 3, t2 = (d + 2) % 3;
+  V[0] = W[0];
+  V[1 + n] = W[1];
+  V[1 + t1] = W[2];
+  V[1 + t2] = W[3];
+  V[4] = W[4];
+  V[5 + n] = W[5];
+  V[5 + t1] = W[6];
+  V[5 + t2] = W[7];
+  if (nvar > 8) V[8] = W[8];
+}
+
+/* ------------------------------------------------------------------------ */
+/* one RK stage operator S(U) = U - sum_d lambda_d (F_{d,i+1/2} - F_{d,i-1/2}) */
+/* (c.2 -> c.3 -> c.5 -> c.6..c.10 -> c.11)                                   */
+/* Up: padded input (interior set; ghosts are filled here).  Out: padded,     */
+/* interior written.                                                          */
+/* ------------------------------------------------------------------------ */
+static int in_star(const grid_t* G, int64_t i, int64_t j, int64_t k) {
+  int outside = (i < 0 || i >= G->n[0]) + (j < 0 || j >= G->n[1]) + (k < 0 || k >= G->n[2]);
+  return outside <= 1;
+}
+
+static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Out, const double lam[3], double ch,
+                    int stage, orc_counters* cnt) {
+  const int nvar = G->nvar;
+  const size_t np = padded_size(G);
+  const size_t plane = (size_t)G->m[0] * G->m[1] * G->m[2];
+
+  /* c.2 */
+  fill_ghosts(c, G, Up);
+
+  /* validity of the stage input (R16): lowest interior linear index */
+  int64_t first_bad = INT64_MAX;
+#pragma omp parallel for reduction(min : first_bad) schedule(static)
+  for (int64_t k = 0; k < G->n[2]; ++k)
+    for (int64_t j = 0; j < G->n[1]; ++j)
+      for (int64_t i = 0; i < G->n[0]; ++i) {
+        double u[9];
+        for (int f = 0; f < nvar; ++f) u[f] = Up[P(G, f, i, j, k)];
+        if (bad_cell(u, nvar) && interior_linear(G, i, j, k) < first_bad) first_bad = interior_linear(G, i, j, k);
+      }
+  if (first_bad != INT64_MAX) {
+    if (cnt->bad_stage < 0) {
+      cnt->bad_stage = stage;
+      cnt->first_bad_cell = first_bad;
+    }
+    return ORC_E_UNPHYSICAL;
+  }
+
+  /* c.3 on every cell the star stencil touches */
+  double* V = (double*)calloc(np, sizeof(double));
+  int64_t floors = 0;
+#pragma omp parallel for reduction(+ : floors) schedule(static)
+  for (int64_t k = -G->g[2]; k < G->n[2] + G->g[2]; ++k)
+    for (int64_t j = -G->g[1]; j < G->n[1] + G->g[1]; ++j)
+      for (int64_t i = -G->g[0]; i < G->n[0] + G->g[0]; ++i) {
+        if (!in_star(G, i, j, k)) continue;
+        double u[9], v[9];
+        for (int f = 0; f < nvar; ++f) u[f] = Up[P(G, f, i, j, k)];
+        int fl = orc_cons2prim(c, u, v);
+        for (int f = 0; f < nvar; ++f) V[P(G, f, i, j, k)] = v[f];
+        if (fl && i >= 0 && i < G->n[0] && j >= 0 && j < G->n[1] && k >= 0 && k < G->n[2]) floors += 1;
+      }
+  cnt->p_floors += floors;
+
+  /* c.5 + c.6..c.10 per active direction; F[d] holds, at cell index i, the flux through face i-1/2 */
+  double* F[3] = {NULL, NULL, NULL};
+  double* Vp = (double*)calloc(np, sizeof(double)); /* q+ : left state of face i+1/2 */
+  double* Vm = (double*)calloc(np, sizeof(double)); /* q- : right state of face i-1/2 */
+  int64_t fallbacks = 0, to_hll = 0;
+  for (int d = 0; d < 3; ++d) {
+    if (!G->act[d]) continue;
+    F[d] = (double*)calloc(np, sizeof(double));
+    int64_t off[3] = {0, 0, 0};
+    off[d] = 1;
+    /* PLM for cells -1..N along d, interior along the other axes */
+    int64_t lo3[3] = {0, 0, 0}, hi3[3] = {G->n[0], G->n[1], G->n[2]};
+    lo3[d] = -1;
+    hi3[d] = G->n[d] + 1;
+#pragma omp parallel for reduction(+ : fallbacks) schedule(static)
+    for (int64_t k = lo3[2]; k < hi3[2]; ++k)
+      for (int64_t j = lo3[1]; j < hi3[1]; ++j)
+        for (int64_t i = lo3[0]; i < hi3[0]; ++i) {
+          double qp[9], qm[9], q0[9];
+          for (int f = 0; f < nvar; ++f) {
+            const double qa = V[P(G, f, i - off[0], j - off[1], k - off[2])];
+            const double qb = V[P(G, f, i, j, k)];
+            const double qc = V[P(G, f, i + off[0], j + off[1], k + off[2])];
+            const double dm = qb - qa, dp = qc - qb;
+            const double s = orc_limited_slope(c->limiter, dm, dp);
+            q0[f] = qb;
+            qp[f] = qb + 0.5 * s;
+            qm[f] = qb - 0.5 * s;
+          }
+          if (!(qp[0] > 0.0 && qm[0] > 0.0 && qp[4] > 0.0 && qm[4] > 0.0)) { /* positivity fallback (R17) */
+            for (int f = 0; f < nvar; ++f) qp[f] = qm[f] = q0[f];
+            const int64_t cd = (d == 0) ? i : (d == 1) ? j : k;
+            if (cd >= 0 && cd < G->n[d]) fallbacks += 1;
+          }
+          for (int f = 0; f < nvar; ++f) {
+            Vp[P(G, f, i, j, k)] = qp[f];
+            Vm[P(G, f, i, j, k)] = qm[f];
+          }
+        }
+    /* faces i-1/2 for i = 0..N: VL = V+[i-1], VR = V-[i] */
+    int64_t fhi[3] = {G->n[0], G->n[1], G->n[2]};
+    fhi[d] = G->n[d] + 1;
+#pragma omp parallel for reduction(+ : to_hll) schedule(static)
+    for (int64_t k = 0; k < fhi[2]; ++k)
+      for (int64_t j = 0; j < fhi[1]; ++j)
+        for (int64_t i = 0; i < fhi[0]; ++i) {
+          double vl[9], vr[9], wl[9], wr[9], fn[9], fx[9];
+          for (int f = 0; f < nvar; ++f) {
+            vl[f] = Vp[P(G, f, i - off[0], j - off[1], k - off[2])];
+            vr[f] = Vm[P(G, f, i, j, k)];
+          }
+          to_normal(d, nvar, vl, wl);
+          to_normal(d, nvar, vr, wr);
+          to_hll += orc_face_flux(c, wl, wr, ch, fn);
+          from_normal(d, nvar, fn, fx);
+          for (int f = 0; f < nvar; ++f) F[d][P(G, f, i, j, k)] = fx[f];
+        }
+  }
+  cnt->plm_fallbacks += fallbacks;
+  cnt->hlld_to_hll += to_hll;
+
+  /* c.11 update: r = lx dFx; r = r + ly dFy; r = r + lz dFz; S(U) = U - r */
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < G->n[2]; ++k)
+    for (int64_t j = 0; j < G->n[1]; ++j)
+      for (int64_t i = 0; i < G->n[0]; ++i)
+        for (int f = 0; f < nvar; ++f) {
+          double r = 0.0;
+          int first = 1;
+          for (int d = 0; d < 3; ++d) {
+            if (!G->act[d]) continue;
+            int64_t o[3] = {0, 0, 0};
+            o[d] = 1;
+            const double dF = F[d][P(G, f, i + o[0], j + o[1], k + o[2])] - F[d][P(G, f, i, j, k)];
+            if (first) {
+              r = lam[d] * dF;
+              first = 0;
+            } else {
+              r = r + lam[d] * dF;
+            }
+          }
+          const size_t q = P(G, f, i, j, k);
+          Out[q] = Up[q] - r;
+        }
+  (void)plane;
+  free(V);
+  free(Vp);
+  free(Vm);
+  for (int d = 0; d < 3; ++d) free(F[d]);
+  return ORC_OK;
+}
+
+void orc_counters_reset(orc_counters* cnt) {
+  memset(cnt, 0, sizeof *cnt);
+  cnt->bad_stage = -1;
+  cnt->first_bad_cell = -1;
+}
+
+int orc_stage(const orc_config* c, const double* U, double* Uout, double dt, double ch, orc_counters* cnt) {
+  grid_t G;
+  int rc = make_grid(c, &G);
+  if (rc) return rc;
+  double lam[3];
+  for (int d = 0; d < 3; ++d) lam[d] = dt / G.dx[d];
+  double* Up = (double*)calloc(padded_size(&G), sizeof(double));
+  double* Out = (double*)calloc(padded_size(&G), sizeof(double));
+  load_interior(&G, U, Up);
+  rc = stage_op(c, &G, Up, Out, lam, ch, 1, cnt);
+  if (rc == ORC_OK) store_interior(&G, Out, Uout);
+  free(Up);
+  free(Out);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.11-c.12: one RK2 step (Heun / SSP-RK2) and the GLM damping               */
+/* ------------------------------------------------------------------------ */
+int orc_step(const orc_config* c, double* U, double dt, double ch, orc_counters* cnt) {
+  grid_t G;
+  int rc = make_grid(c, &G);
+  if (rc) return rc;
+  if (!(dt > 0.0) || !isfinite(dt)) return ORC_E_ARG;
+  if (c->glm && !(ch > 0.0)) return ORC_E_ARG;
+  /* host scalars (R4) */
+  double lam[3], dxmin = INFINITY;
+  for (int d = 0; d < 3; ++d) {
+    lam[d] = dt / G.dx[d];
+    if (G.act[d] && G.dx[d] < dxmin) dxmin = G.dx[d];
+  }
+  const double damp = exp(-((c->glm_alpha * ch) * dt) / dxmin);
+
+  const size_t np = padded_size(&G);
+  double* Un = (double*)calloc(np, sizeof(double));
+  double* Us = (double*)calloc(np, sizeof(double));
+  double* Uss = (double*)calloc(np, sizeof(double));
+  load_interior(&G, U, Un);
+  rc = stage_op(c, &G, Un, Us, lam, ch, 1, cnt); /* U* = S(U^n) */
+  if (rc == ORC_OK) rc = stage_op(c, &G, Us, Uss, lam, ch, 2, cnt); /* U** = S(U*) */
+  if (rc == ORC_OK) {
+    for (int f = 0; f < G.nvar; ++f)
+      for (int64_t k = 0; k < G.n[2]; ++k)
+        for (int64_t j = 0; j < G.n[1]; ++j)
+          for (int64_t i = 0; i < G.n[0]; ++i) {
+            const size_t q = P(&G, f, i, j, k);
+            double u = 0.5 * (Un[q] + Uss[q]); /* U^{n+1} = (U^n + U**)/2 */
+            if (f == 8) u = u * damp;          /* c.12 psi damping, once per step */
+            Uss[q] = u;
+          }
+    store_interior(&G, Uss, U);
+  }
+  free(Un);
+  free(Us);
+  free(Uss);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.13 CFL dt and the GLM speed c_h                                          */
+/* ------------------------------------------------------------------------ */
+int orc_compute_dt(const orc_config* c, const double* U, double* dt, double* ch, orc_counters* cnt) {
+  grid_t G;
+  int rc = make_grid(c, &G);
+  if (rc) return rc;
+  double idx[3];
+  for (int d = 0; d < 3; ++d) idx[d] = 1.0 / G.dx[d];
+  const int nvar = G.nvar;
+  const size_t ncell = (size_t)G.n[0] * G.n[1] * G.n[2];
+  double M = 0.0, S = 0.0;
+  int64_t first_bad = INT64_MAX;
+#pragma omp parallel for reduction(max : M, S) reduction(min : first_bad) schedule(static)
+  for (int64_t k = 0; k < G.n[2]; ++k)
+    for (int64_t j = 0; j < G.n[1]; ++j)
+      for (int64_t i = 0; i < G.n[0]; ++i) {
+        const size_t lin = (size_t)interior_linear(&G, i, j, k);
+        double u[9], v[9];
+        for (int f = 0; f < nvar; ++f) u[f] = U[(size_t)f * ncell + lin];
+        if (bad_cell(u, nvar)) {
+          if ((int64_t)lin < first_bad) first_bad = (int64_t)lin;
+          continue;
+        }
+        orc_cons2prim(c, u, v); /* floor applies; not counted (c.16) */
+        double inv = 0.0, smax = 0.0;
+        int first = 1;
+        for (int d = 0; d < 3; ++d) {
+          if (!G.act[d]) continue;
+          const double cf = orc_fast_speed(c->gamma, v[0], v[4], v[5 + d], v[5 + (d + 1) % 3], v[5 + (d + 2) % 3]);
+          const double s = fabs(v[1 + d]) + cf;
+          if (first) {
+            inv = s * idx[d];
+            smax = s;
+            first = 0;
+          } else {
+            inv = inv + s * idx[d];
+            smax = fmax(smax, s);
+          }
+        }
+        if (inv > M) M = inv;
+        if (smax > S) S = smax;
+      }
+  if (first_bad != INT64_MAX) {
+    if (cnt->bad_stage < 0) {
+      cnt->bad_stage = 0;
+      cnt->first_bad_cell = first_bad;
+    }
+    return ORC_E_UNPHYSICAL;
+  }
+  if (!isfinite(M) || !(M > 0.0)) return ORC_E_UNPHYSICAL;
+  *dt = c->cfl / M;
+  *ch = S;
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* c.14 driver loop                                                           */
+/* ------------------------------------------------------------------------ */
+int orc_run(const orc_config* c, double* U, int64_t nsteps, double t_end, double* dt_log, int64_t* steps_done,
+            orc_counters* cnt) {
+  double t = 0.0;
+  int64_t n = 0;
+  int rc = ORC_OK;
+  while (n < nsteps && (t_end <= 0.0 || t < t_end)) {
+    double dt, ch;
+    rc = orc_compute_dt(c, U, &dt, &ch, cnt);
+    if (rc) break;
+    if (t_end > 0.0 && t + dt > t_end) dt = t_end - t;
+    rc = orc_step(c, U, dt, ch, cnt);
+    if (rc) break;
+    if (dt_log) dt_log[n] = dt;
+    t = t + dt;
+    n += 1;
+  }
+  if (steps_done) *steps_done = n;
+  return rc;
+}
+
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

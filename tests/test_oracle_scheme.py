@@ -1,0 +1,233 @@
+"""Whole-scheme pins of the CPU oracle: textbook exact
+solutions, conservation, symmetry, convergence order, GLM behaviour, invariance properties.
+None of these compares the oracle with itself or with the CUDA path."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_24175_b200 import inputs as I
+
+from exact_riemann import sample as exact_sample, star as exact_star
+from test_oracle_pins import cf_textbook
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def prims(p, U):
+    """primitive variables of every interior cell via textbook algebra (not the oracle)."""
+    r = U[0]
+    v = U[1:4] / r
+    B = U[5:8]
+    pr = (p.gamma - 1) * (U[4] - 0.5 * r * (v * v).sum(0) - 0.5 * (B * B).sum(0))
+    return r, v, pr, B
+
+
+# ---------------------------------------------------------------------------------------------
+# Sod: exact Riemann solution (Toro Test 1)
+# ---------------------------------------------------------------------------------------------
+def test_exact_solver_matches_toro_table():
+    g = json.load(open(os.path.join(GOLD, "sod_toro_test1.json")))
+    ps, us = exact_star(1.0, 0.0, 1.0, 0.125, 0.0, 0.1, 1.4)
+    assert abs(ps - g["p_star"]) < 1e-5 and abs(us - g["u_star"]) < 1e-5
+
+
+@pytest.mark.parametrize("riemann", [I.HLL, I.HLLD])
+def test_sod_plateaus_and_convergence(riemann):
+    g = json.load(open(os.path.join(GOLD, "sod_toro_test1.json")))
+    errs = []
+    for n in (128, 256, 512):
+        p = I.sod(n, riemann=riemann)
+        o = oracle.Oracle(p, I.sod_ic(p))
+        o.run(100000, p.t_end)
+        assert abs(o.t - 0.2) < 1e-14
+        r, v, pr, _ = prims(p, o.U)
+        x = I.centres(p, 0)
+        ex = exact_sample(x, 0.2, 0.5, 1.0, 0.0, 1.0, 0.125, 0.0, 0.1, 1.4)
+        errs.append(np.abs(r[0, 0] - ex[0]).mean())
+        if n == 512:
+            def at(xx):
+                return int(xx * n)
+            # plateaus: left star region (tail 0.486 .. contact 0.685), right star (0.685 .. shock 0.850)
+            for xx in (0.56, 0.60, 0.64):
+                assert abs(r[0, 0, at(xx)] - g["rho_star_left"]) < 1e-3
+                assert abs(pr[0, 0, at(xx)] - g["p_star"]) < 1e-3
+                assert abs(v[0, 0, 0, at(xx)] - g["u_star"]) < 1e-3
+            for xx in (0.74, 0.78, 0.81):
+                assert abs(r[0, 0, at(xx)] - g["rho_star_right"]) < 1e-3
+                assert abs(pr[0, 0, at(xx)] - g["p_star"]) < 1e-3
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] < 4e-3
+
+
+# ---------------------------------------------------------------------------------------------
+# Brio-Wu (BASELINE configs[0]): exact budgets while the waves are interior
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("riemann,limiter", [(I.HLL, I.MC), (I.HLLD, I.MC), (I.HLL, I.MINMOD)])
+def test_brio_wu_budgets(riemann, limiter):
+    g = json.load(open(os.path.join(GOLD, "brio_wu_setup.json")))
+    p = I.brio_wu(512, riemann=riemann, limiter=limiter)
+    U0 = I.brio_wu_ic(p)
+    o = oracle.Oracle(p, U0)
+    dt0, _ = o.compute_dt()
+    # first dt from the textbook fast speed of the right state (1 ulp)
+    ref = 0.4 / (512 * cf_textbook(2.0, 0.125, 0.1, 0.75, -1.0, 0.0))
+    assert abs(dt0 - ref) <= 2 * np.finfo(float).eps * ref
+    assert abs(cf_textbook(2.0, 0.125, 0.1, 0.75, -1.0, 0.0) - g["cf_right"]) < 1e-5
+    log = o.run(100000, p.t_end)
+    assert 480 < len(log) < 500
+    dx = 1.0 / 512
+    U = o.U
+    assert np.all(U[5] == 0.75)                       # Bx bitwise constant (flux exactly 0)
+    for f in (0, 4, 6):                               # rho, E, By: boundary fluxes cancel (outflow, uniform ends)
+        assert abs((U[f].sum() - U0[f].sum()) * dx) <= 1e-14 * max(1.0, np.abs(U0[f]).sum() * dx)
+    assert np.all(U[3] == 0) and np.all(U[7] == 0)   # mz, Bz: fluxes are exactly 0 (vz = Bz = 0)
+    mx = U[1].sum() * dx
+    assert abs(mx - g["momentum_budget_t0p1"]) <= 1e-14
+    my = U[2].sum() * dx                              # boundary flux -Bx*By: d/dt = -0.75 - 0.75
+    assert abs(my - g["momentum_y_budget_t0p1"]) <= 1e-14
+    assert o.counters()["p_floors"] == 0
+
+
+# ---------------------------------------------------------------------------------------------
+# periodic conservation, symmetry, GLM
+# ---------------------------------------------------------------------------------------------
+def test_ot2d_conservation_and_point_symmetry():
+    p = I.orszag_tang_2d(64)
+    U0 = I.orszag_tang_2d_ic(p)
+    o = oracle.Oracle(p, U0)
+    o.run(60)
+    U = o.U
+    for f in range(8):
+        tot0, tot = U0[f].sum(), U[f].sum()
+        scale = np.abs(U0[f]).sum()
+        assert abs(tot - tot0) <= 1e-13 * scale, f
+    # point symmetry about the centre: scalars even, vectors odd (OT-2D)
+    def rot(a):
+        return a[:, ::-1, ::-1]
+    for f, sgn in ((0, 1), (4, 1), (1, -1), (2, -1), (5, -1), (6, -1)):
+        a = U[f]
+        assert np.abs(a - sgn * rot(a)).max() <= 1e-12 * np.abs(a).max(), f
+    assert np.abs(U[3]).max() == 0 and np.abs(U[7]).max() == 0  # 2D: mz, Bz stay exactly zero
+
+
+def _divb_rms(p, U):
+    dx, dy = 1.0 / p.n[0], 1.0 / p.n[1]
+    bx, by = U[5, 0], U[6, 0]
+    div = (np.roll(bx, -1, 1) - np.roll(bx, 1, 1)) / (2 * dx) + (np.roll(by, -1, 0) - np.roll(by, 1, 0)) / (2 * dy)
+    return np.sqrt((div * dx) ** 2).mean() / np.sqrt((bx * bx + by * by).mean())
+
+
+@pytest.mark.slow
+def test_glm_reduces_divergence():
+    out = {}
+    for glm in (1, 0):
+        p = I.orszag_tang_2d(64, glm=glm)
+        o = oracle.Oracle(p, I.orszag_tang_2d_ic(p))
+        o.run(100000, 0.5)
+        out[glm] = _divb_rms(p, o.U)
+    assert out[1] <= 0.5 * out[0]
+    assert out[1] <= 2e-2
+
+
+def test_glm_fixed_point_and_damping():
+    """uniform state: every flux difference is exactly 0, so U^{n+1} = U^n bitwise except
+    psi = psi0 * damp once per step (Mignone & Tzeferacos 2010 parabolic term)."""
+    p = I.orszag_tang_3d(8)
+    U = I.prim_to_cons_ic(p, 1.3, 0.2, -0.1, 0.3, 0.7, 0.4, 0.5, -0.6, psi=0.0)
+    o = oracle.Oracle(p, U)
+    dt, ch = o.compute_dt()
+    o.step(dt, ch)
+    assert np.array_equal(o.U, U)  # psi = 0 stays 0 (fixed point)
+    U[8] = 0.05
+    o = oracle.Oracle(p, U)
+    dt, ch = o.compute_dt()
+    o.step(dt, ch)
+    assert np.array_equal(o.U[:8], U[:8])
+    damp = math.exp(-(0.1 * ch * dt) / (1.0 / 8))
+    assert np.allclose(o.U[8], 0.05 * damp, rtol=4e-16, atol=0)
+    assert np.all(o.U[8] < 0.05)
+    # uniform-state dt closed form: dt = cfl / sum_d (|v_d| + cf_d)/dx_d
+    r, v, pr, B = 1.3, np.array([0.2, -0.1, 0.3]), 0.7, np.array([0.4, 0.5, -0.6])
+    s = [abs(v[d]) + cf_textbook(p.gamma, r, pr, B[d], B[(d + 1) % 3], B[(d + 2) % 3]) for d in range(3)]
+    assert abs(dt - 0.4 / (8 * sum(s))) <= 1e-14 * dt
+    assert abs(ch - max(s)) <= 1e-14 * ch
+
+
+def test_1d_embedded_in_3d_bitwise():
+    """A 1D problem embedded in a 3D grid uniform along y and z: the y/z flux differences are
+    exactly 0.0, so the 3D step equals the 1D step bitwise (same dt, ch): pins the 3D assembly
+    (c.11 order x, y, z) and the frame permutations."""
+    p1 = I.brio_wu(64).replace(glm=1)
+    U1 = I.brio_wu_ic(p1)
+    p3 = p1.replace(n=(64, 4, 4))
+    U3 = np.broadcast_to(U1, (9, 4, 4, 64)).copy()
+    o1, o3 = oracle.Oracle(p1, U1), oracle.Oracle(p3, U3)
+    for _ in range(5):
+        dt, ch = o1.compute_dt()
+        o1.step(dt, ch)
+        o3.step(dt, ch)
+    assert np.array_equal(np.broadcast_to(o1.U, (9, 4, 4, 64)), o3.U)
+
+
+def test_thread_count_invariance_bitwise():
+    p = I.orszag_tang_3d(16)
+    U = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    res = []
+    for nt in (1, 3):
+        oracle.set_num_threads(nt)
+        o = oracle.Oracle(p, U)
+        log = o.run(3)
+        res.append((o.U.copy(), log, o.counters()))
+    oracle.set_num_threads(os.cpu_count() or 1)
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+    assert res[0][2] == res[1][2]
+
+
+# ---------------------------------------------------------------------------------------------
+# convergence on exact smooth solutions (north star: "second-order convergence on a linear Alfven wave")
+# ---------------------------------------------------------------------------------------------
+def _alfven_errors(make, ic, ns, limiter, amp, field):
+    errs = []
+    for n in ns:
+        p = make(n, limiter=limiter)
+        U0 = ic(p)
+        o = oracle.Oracle(p, U0)
+        o.run(10 ** 6, p.t_end)
+        assert abs(o.t - p.t_end) < 1e-12
+        errs.append(np.abs(o.U[field] - U0[field]).mean() / amp)  # exact solution at t = 1 is the IC
+    return errs
+
+
+@pytest.mark.parametrize("limiter,order_min", [(I.MC, 1.9), (I.MINMOD, 1.8)])
+def test_linear_alfven_second_order(limiter, order_min):
+    errs = _alfven_errors(I.linear_alfven, I.linear_alfven_ic, (32, 64, 128, 256), limiter, 1e-6, 6)
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert orders[-1] >= order_min, (errs, orders)
+    assert all(o > 1.5 for o in orders), orders
+
+
+@pytest.mark.parametrize("limiter,order_min", [(I.MC, 1.9), (I.MINMOD, 1.8)])
+def test_cpa_second_order(limiter, order_min):
+    errs = _alfven_errors(I.cpa_1d, I.cpa_1d_ic, (32, 64, 128, 256), limiter, 0.1, 6)
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert orders[-1] >= order_min, (errs, orders)
+    if limiter == I.MC:
+        assert errs[-1] <= 6e-4
+
+
+def test_unphysical_state_reported():
+    p = I.orszag_tang_3d(8)
+    U = I.orszag_tang_3d_ic(p)
+    U[0, 3, 2, 5] = -1.0
+    U[0, 5, 0, 1] = 0.0
+    o = oracle.Oracle(p, U)
+    with pytest.raises(oracle.OracleError) as e:
+        o.compute_dt()
+    assert e.value.rc == 6
+    c = e.value.counters.as_dict()
+    assert c["bad_stage"] == 0 and c["first_bad_cell"] == (3 * 8 + 2) * 8 + 5
