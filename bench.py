@@ -1,0 +1,295 @@
+#!/usr/bin/env python
+"""bench.py — zone-updates/s of the fp64 3D ideal-MHD Godunov step on B200 (BASELINE.json metric).
+
+Workload: BASELINE configs[2], 3D Orszag-Tang 256^3 periodic, PLM-MC + HLLD + GLM,
+SSP-RK2, CFL 0.4 — the single-GPU roofline run — per GPU.  With N GPUs the job is weak-scaled:
+a 256 x 256 x (256 N) periodic box (z extent N), one 256^3 z-slab per rank, halo exchange by NCCL
+send/recv and the dt reduction by ncclAllReduce(max) inside the library.
+
+A step is one user-loop iteration: dt = mhd_compute_dt() (k_dt + 16-byte read-back) then
+mhd_step(dt) (z ghost planes + 2 fused stage kernels).  A zone-update is one interior cell
+advanced one full step (R25).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mhd|reference]
+
+--impl reference times the CPU oracle (the reference arm of this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "zone-updates/sec (fp64 3D ideal MHD) at 1/2/4/8 B200; HBM GB/s fraction"
+UNIT = "zone-updates/s"
+NV = 9
+# algorithmic HBM bytes of one fused stage launch per interior cell:
+# stage 1 reads U^n, writes U*; stage 2 reads U*, reads U^n, writes U^n+1  -> 144 + 216 = 360 B/zu
+STAGE_BYTES_PER_CELL = {1: 2 * NV * 8, 2: 3 * NV * 8}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def build_problem(n_gpus: int, n: int):
+    from paper_2510_24175_b200 import inputs as I
+    return I.orszag_tang_3d(n, nz=n * n_gpus, z_extent=float(n_gpus))
+
+
+def cpu_info():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = [l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")]
+        return model[0] if model else "unknown"
+    except Exception:
+        return "unknown"
+
+
+def oracle_sample(n: int, nz_s: int, steps: int, warmup: int):
+    """The CPU oracle, as it stands, on a bounded sample of the workload: the first nz_s planes of
+    the n^3 OT-3D initial condition as a periodic n x n x nz_s slab (same per-cell work)."""
+    import oracle
+    from paper_2510_24175_b200 import inputs as I
+    full = I.orszag_tang_3d(n)
+    p = full.replace(n=(n, n, nz_s), hi=(1.0, 1.0, nz_s / n))
+    U = I.orszag_tang_3d_ic(full, z_range=(0, nz_s))
+    o = oracle.Oracle(p, U)
+    for _ in range(warmup):
+        dt, ch = o.compute_dt()
+        o.step(dt, ch)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        dt, ch = o.compute_dt()
+        o.step(dt, ch)
+    el = time.perf_counter() - t0
+    return p.cells * steps / el, el, oracle.num_threads(), p
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n, nz_s = args.n, max(4, args.n // 8)
+    v, el, cores, p = oracle_sample(n, nz_s, args.steps, args.warmup)
+    sample = (f"CPU oracle (oracle/mhd_oracle.c, gcc -O2 -ffp-contract=off, OpenMP {cores} threads), "
+              f"{args.steps} timed steps after {args.warmup} warm-up of a {n}x{n}x{nz_s} periodic slab of the "
+              f"{n}^3 OT-3D IC (1/{n // nz_s} of the workload per step)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"ot3d_{n}", "cells_per_step": p.cells, "sample": f"{n}x{n}x{nz_s}",
+                       "parallelism": "host cores"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_info()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mhd", choices=["mhd", "reference"])
+    ap.add_argument("--n", type=int, default=256, help="cells per axis per GPU (configs[2]: 256)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-planes", type=int, default=32)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "mhd" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2510_24175_b200 import inputs as I
+    from paper_2510_24175_b200 import mhd
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    p = build_problem(world, args.n)
+    nz_loc = p.n[2] // world
+    nccl_id = None
+    if world > 1:
+        obj = [mhd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    s = mhd.Solver(p, rank=rank, nranks=world, device=local_rank, nccl_id=nccl_id)
+    stream = torch.cuda.current_stream()
+    s.set_stream(stream)
+    U0 = I.orszag_tang_3d_ic(p, z_range=(rank * nz_loc, (rank + 1) * nz_loc))
+    U0d = torch.from_numpy(U0).cuda()
+    s.set_state(U0d)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        s.step(s.compute_dt())
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the library's stream = torch's current stream)
+    s.profile_enable(True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.step(s.compute_dt())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    prof = s.profile_read()
+    s.profile_enable(False)
+    ms_max = max_over_ranks(ms)
+    cells = p.cells
+    value = cells * args.steps / (ms_max * 1e-3)
+    diag = s.diag()
+
+    # ---- roofline of the dominant kernel (fused stage kernel)
+    pk, pk_kind = peaks()
+    stage_ms, stage_n = prof["stage"]
+    dt_ms, dt_n = prof["dt"]
+    cells_loc = p.cells // world
+    stage_bytes = cells_loc * (STAGE_BYTES_PER_CELL[1] + STAGE_BYTES_PER_CELL[2]) / 2.0  # per launch (avg)
+    stage_avg_s = stage_ms * 1e-3 / max(stage_n, 1)
+    achieved_gbs = stage_bytes / stage_avg_s / 1e9
+    roof = {"bound": "alu", "kernel": "k_stage (fused cons2prim+PLM+GLM+HLLD+update)",
+            "hbm": {"achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                    "frac": achieved_gbs / pk.get("hbm_gbs", 6537.3), "peak_kind": pk_kind,
+                    "algorithmic_bytes_per_launch": stage_bytes},
+            "stage_ms_per_launch": stage_avg_s * 1e3, "stage_share_of_step": stage_ms / max(ms, 1e-9),
+            "dt_ms_per_launch": dt_ms / max(dt_n, 1), "traffic": None}
+    roof.update({"achieved": achieved_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                 "frac": achieved_gbs / pk.get("hbm_gbs", 6537.3), "bound": "hbm"})
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.from_numpy(U0).pin_memory()
+        Uo = torch.empty_like(Uh).pin_memory()
+        ke = max(1, min(args.steps, 5))
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ke):
+            s.set_state(Uh)
+            s.step(s.compute_dt())
+            s.get_state(Uo)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": cells * ke / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": Uh.numel() * 8,
+               "d2h_bytes_per_step": Uo.numel() * 8, "steps": ke,
+               "what": "per step: mhd_set_state(pinned host U) + mhd_compute_dt + mhd_step + mhd_get_state(pinned host)"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nz_s = min(args.cpu_planes, args.n)
+        v, el, cores, pp = oracle_sample(args.n, nz_s, 1, 0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_info(),
+               "sample": f"1 step (compute_dt + RK2 step) of a {args.n}x{args.n}x{nz_s} periodic slab of the "
+                         f"{args.n}^3 OT-3D IC, {el:.1f} s on {cores} OpenMP threads"}
+
+    s.destroy()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"ot3d_{args.n}^3_per_gpu (BASELINE configs[2]; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
+                           "scheme": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4", "cells": cells,
+                           "parallelism": f"z-slab x{world}", "l2": "inputs larger than L2 (2 x 1.27 GB arrays per GPU)"},
+                "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * 3,
+                "e2e": e2e, "cpu_baseline": cpu, "diag": diag,
+                "lib": mhd.version()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

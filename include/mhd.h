@@ -1,0 +1,171 @@
+/*
+ * mhd.h — C ABI of libmhd: a B200-native (sm_100a) fp64 ideal-MHD Godunov step.
+ *
+ * The operation is gPLUTO's data-parallel hot path (arxiv 2510.24175): "boundary
+ * exchange/calculation, mapping of the conservative vectors to primitive vectors,
+ * reconstruction ... of the cells interfaces values, solving Riemann problem to calculate
+ * the fluxes at the interfaces, computing the right hand side of the conservation law",
+ * repeated for each Runge-Kutta stage (§3.2), with divergence cleaning
+ * in double precision.  The exact recipe (PLM minmod/MC,
+ * HLL/HLLD, GLM, SSP-RK2, CFL dt) is DESIGN.md §3; the call set is BASELINE.json's north
+ * star ("mhd_create(grid,gamma,cfl,bc), mhd_set_state, mhd_compute_dt, mhd_step,
+ * mhd_get_state, mhd_destroy") and SURVEY.md §8(b).
+ *
+ * Conventions
+ *  - extern "C", fp64 only; every call returns an int status (MHD_OK = 0); nothing throws.
+ *  - Layout at the ABI: U[f][z][y][x], x fastest, this rank's interior cells only,
+ *    nvar = 8 + (glm != 0) fields in the order (rho, mx, my, mz, E, Bx, By, Bz, psi).
+ *    Internally the library keeps padded [z][f][y][x] arrays with 2 ghost cells per side
+ *    on every active axis.
+ *  - Ownership: the caller owns every host or device buffer it passes; the context owns
+ *    the device state it allocates and its NCCL communicator.
+ *  - Asynchrony: mhd_step is asynchronous with respect to the host (it enqueues on the
+ *    context's stream); mhd_compute_dt and mhd_get_state synchronise.
+ *  - Errors are sticky: after MHD_E_UNPHYSICAL, MHD_E_CUDA or MHD_E_NCCL every call except
+ *    mhd_get_state / mhd_get_diag / mhd_last_error / mhd_destroy returns MHD_E_STATE until
+ *    the next successful mhd_set_state.
+ *  - Collective semantics: with nranks > 1, mhd_create, mhd_compute_dt, mhd_step and
+ *    mhd_destroy must be called by every rank in the same order (as with NCCL).
+ *  - A context is not thread-safe; different contexts are independent.
+ */
+#ifndef MHD_H
+#define MHD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MHD_OK = 0,
+  MHD_E_ARG = 1,        /* invalid argument (checked synchronously) */
+  MHD_E_STATE = 2,      /* context in a sticky error state, or call out of order */
+  MHD_E_CUDA = 3,       /* CUDA runtime error (message in mhd_last_error) */
+  MHD_E_NCCL = 4,       /* NCCL error or timeout */
+  MHD_E_NOMEM = 5,      /* device allocation failed */
+  MHD_E_UNPHYSICAL = 6  /* rho <= 0 or non-finite state (see mhd_diag.first_bad_cell) */
+};
+enum { MHD_BC_PERIODIC = 0, MHD_BC_OUTFLOW = 1 };
+enum { MHD_LIM_MINMOD = 0, MHD_LIM_MC = 1 };
+enum { MHD_RS_HLL = 0, MHD_RS_HLLD = 1 };
+
+/* Global grid. n[d] == 1 makes axis d inactive (1D uses x; 2D uses x, y).  Active axes
+ * need n[d] >= 4.  lo < hi on every axis.  DESIGN.md §3.1. */
+typedef struct {
+  int64_t n[3];
+  double lo[3], hi[3];
+} mhd_grid;
+
+/* Boundary condition per axis and side.  Periodic must be set on both
+ * sides of an axis.  With nranks > 1 the z axis must be periodic (slab ring). */
+typedef struct {
+  int32_t lo[3], hi[3];
+} mhd_bc;
+
+/* Scheme selection.  NULL => MC, HLLD, GLM on, alpha 0.1, floor 1e-12.
+ * GLM is required when two or more axes are active. */
+typedef struct {
+  int32_t limiter;   /* MHD_LIM_* */
+  int32_t riemann;   /* MHD_RS_* */
+  int32_t glm;       /* 1: nvar = 9 with the psi field and c_h coupling */
+  int32_t reserved;
+  double glm_alpha;  /* psi damping exp(-alpha*ch*dt/dx_min), R12 */
+  double p_floor;    /* pressure floor on primitives (counted), R16 */
+} mhd_scheme;
+
+/* Multi-GPU: z-slab decomposition over nranks GPUs.  NULL => 1 GPU, the
+ * current CUDA device.  nranks must divide n[2] with n[2]/nranks >= 2.  nccl_id comes from
+ * mhd_nccl_get_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed). */
+typedef struct {
+  int32_t rank, nranks, device, reserved;
+  uint8_t nccl_id[128];
+} mhd_dist;
+
+/* Diagnostics (sums over all ranks after a synchronising call).  Counter ownership is
+ * DESIGN.md §3.13. */
+typedef struct {
+  int64_t steps;          /* mhd_step calls completed */
+  int64_t p_floors;       /* (interior cell, stage) pressure floors */
+  int64_t plm_fallbacks;  /* (interior cell, direction, stage) first-order fallbacks */
+  int64_t hlld_to_hll;    /* (face, stage) HLLD -> HLL fallbacks */
+  int64_t first_bad_cell; /* lowest global interior linear index (z*ny+y)*nx+x, or -1 */
+  int32_t bad_stage;      /* 0 dt pass, 1/2 RK stage, -1 none */
+  int32_t reserved;
+} mhd_diag;
+
+typedef struct mhd_ctx mhd_ctx; /* opaque; created by mhd_create, freed by mhd_destroy */
+
+/* rank 0 only; 128 bytes to broadcast to the other ranks before mhd_create. */
+int mhd_nccl_get_unique_id(uint8_t out[128]);
+
+/* Validates the arguments (MHD_E_ARG), plans the slab, allocates the two padded state
+ * arrays (U^n and U*) on the device and, for nranks > 1, creates the NCCL communicator
+ * (collective).  gamma > 1, 0 < cfl < 1.  *out receives the context (NULL on failure). */
+int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
+               const mhd_scheme* scheme, const mhd_dist* dist, mhd_ctx** out);
+
+/* Enqueue all further work on this CUDA stream (cudaStream_t as void*; NULL = default).
+ * E.g. torch.cuda.current_stream().cuda_stream. */
+int mhd_set_stream(mhd_ctx* ctx, void* cuda_stream);
+
+/* This rank's interior block in global cell coordinates. */
+int mhd_local_box(const mhd_ctx* ctx, int64_t off[3], int64_t ext[3]);
+
+/* Bytes of device memory the context holds. */
+int mhd_device_bytes(const mhd_ctx* ctx, size_t* bytes);
+
+/* Copy a state in: U is [nvar][ext_z][ext_y][ext_x] (mhd_local_box), host memory when
+ * on_device == 0 (pinned host memory makes the copy asynchronous-capable), device memory
+ * otherwise.  Validates rho > 0, p > 0 and finiteness on the device (MHD_E_UNPHYSICAL with
+ * the first bad cell); clears a sticky error; invalidates the cached dt. Synchronising. */
+int mhd_set_state(mhd_ctx* ctx, const double* U, int32_t on_device);
+
+/* Copy the state out, same layout as mhd_set_state.  Synchronising. */
+int mhd_get_state(mhd_ctx* ctx, double* U, int32_t on_device);
+
+/* CFL dt of the current state (row a6): dt = cfl / max_cells sum_d
+ * (|v_d| + c_f,d)/dx_d, global over ranks (collective); also caches c_h = max_cells
+ * max_d (|v_d| + c_f,d) for the next mhd_step.  Reports an unphysical state found by the
+ * preceding mhd_step.  Host-synchronising (16-byte read-back). */
+int mhd_compute_dt(mhd_ctx* ctx, double* dt);
+
+/* One SSP-RK2 step (rows a1-a5) with the given dt > 0 and the c_h cached
+ * by the last mhd_compute_dt on this state (recomputed if the state changed since).
+ * Collective with nranks > 1; asynchronous with respect to the host.  Also produces the
+ * partial maxima the next mhd_compute_dt needs. */
+int mhd_step(mhd_ctx* ctx, double dt);
+
+/* Counters and the unphysical-state record (synchronising; collective when nranks > 1
+ * only through mhd_compute_dt, which refreshes the global sums). */
+int mhd_get_diag(const mhd_ctx* ctx, mhd_diag* diag);
+
+/* Last error message of this context (valid until the next call on it); never NULL. */
+const char* mhd_last_error(const mhd_ctx* ctx);
+
+/* Frees what the context allocated, including its NCCL communicator.  NULL-safe. */
+void mhd_destroy(mhd_ctx* ctx);
+
+/* Test-only: the face solve of n independent face pairs in the
+ * normal frame.  VL, VR, F are DEVICE pointers to [n][nvar] rows; ch is the GLM speed.
+ * Enqueued on the context's stream, synchronised before return. *n_hll receives the
+ * number of HLLD -> HLL fallbacks (may be NULL). */
+int mhd_debug_face_flux(mhd_ctx* ctx, const double* VL, const double* VR, int64_t n, double ch,
+                        double* F, int64_t* n_hll);
+
+/* Kernel timing (measurement support for bench.py): while enabled, every
+ * launch of the fused stage kernel and of the dt kernel is bracketed by CUDA events on the
+ * context's stream.  mhd_profile_read synchronises, adds up the event intervals recorded
+ * since enable, and returns total milliseconds and launch counts per kernel class
+ * (index 0: stage kernel, 1: dt kernel).  Enabling resets the totals. */
+int mhd_profile_enable(mhd_ctx* ctx, int32_t enable);
+int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
+
+/* Library build identity, e.g. "libmhd sm_100a fused-v1". */
+const char* mhd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHD_H */

@@ -1,0 +1,56 @@
+"""Build libmhd.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+Flags: --fmad=false (no FMA contraction: DESIGN.md R-ARITH, bitwise parity with the oracle),
+-lineinfo (ncu source view), linked against the NCCL 2.28 that torch loads
+(site-packages/nvidia/nccl)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libmhd.so")
+SOURCES = ["mhd_kernels.cu", "mhd_api.cu"]
+DEPS = SOURCES + ["mhd_device.cuh", "mhd_kernels.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia-nccl wheel not found (torch's NCCL)")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def needs_build() -> bool:
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    srcs = [os.path.join(CSRC, s) for s in DEPS] + [os.path.join(ROOT, "include", "mhd.h"), __file__]
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return OUT
+    inc, lib = nccl_dirs()
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+           "-shared", "-I", os.path.join(ROOT, "include"), "-I", inc,
+           *[os.path.join(CSRC, s) for s in SOURCES],
+           "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", OUT + ".tmp"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

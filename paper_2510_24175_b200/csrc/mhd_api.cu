@@ -1,0 +1,582 @@
+// mhd_api.cu — host side of libmhd: the C ABI declared in include/mhd.h.
+//
+// Owns the device state (two padded fp64 arrays, U^n and U*), the stream, the z-slab plan
+// and the NCCL communicator; sequences one SSP-RK2 step as
+//   [z ghost planes of U^n] -> k_stage(stage 1) -> [z ghost planes of U*] -> k_stage(stage 2)
+// (§3.2: boundary exchange, then the offloaded per-cell/per-face work, per
+// Runge-Kutta stage; the boundary exchange is the only inter-GPU step), and
+// the CFL reduction as k_dt -> ncclAllReduce(max) -> 16-byte read-back.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/mhd.h"
+#include "mhd_kernels.h"
+
+using mhd::DtArgs;
+using mhd::StageArgs;
+using mhd::StageConsts;
+
+struct mhd_ctx {
+  // problem
+  int64_t n[3];
+  double lo[3], hi[3], dx[3], dxmin;
+  int dim, nv;
+  int bc_lo[3], bc_hi[3];
+  mhd_scheme scheme;
+  double gamma, cfl;
+  // decomposition
+  int rank, nranks, device;
+  int nx, ny, nzl, gz;
+  long long zoff;
+  int up, down;  // ring neighbours along z (-1: none)
+  // device state
+  double* U0 = nullptr;  // U^n
+  double* U1 = nullptr;  // U*
+  size_t arr_elems = 0;
+  unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..7] bad slots, [16] debug
+  unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (same 8 entries)
+  unsigned long long* hbuf = nullptr;  // pinned host mirror
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  int nsm = 148;
+  int kz = 32;
+  // cached step state
+  double ch = 0.0;
+  bool ch_valid = false;
+  bool has_state = false;
+  int sticky = MHD_OK;
+  mhd_diag diag;
+  char err[512];
+  // kernel timing (mhd_profile_*)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;  // one entry per recorded (start, stop) pair
+  double prof_ms[2] = {0, 0};
+  int64_t prof_n[2] = {0, 0};
+};
+
+namespace {
+
+const char* kVersion = "libmhd sm_100a fused-stage-v1 (fp64, --fmad=false)";
+
+int set_err(mhd_ctx* c, int code, const char* fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof c->err, fmt, ap);
+    va_end(ap);
+    if (code == MHD_E_UNPHYSICAL || code == MHD_E_CUDA || code == MHD_E_NCCL) c->sticky = code;
+  }
+  return code;
+}
+
+#define CUDA_OR_RETURN(ctx, call)                                                                   \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return set_err(ctx, MHD_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_OR_RETURN(ctx, call)                                                                     \
+  do {                                                                                                 \
+    ncclResult_t r_ = (call);                                                                          \
+    if (r_ != ncclSuccess) return set_err(ctx, MHD_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+size_t plane_elems(const mhd_ctx* c) { return (size_t)c->nv * c->nx * c->ny; }
+
+int check_sticky(mhd_ctx* c) {
+  if (c->sticky != MHD_OK)
+    return set_err(c, MHD_E_STATE, "context in error state %d; call mhd_set_state to recover", c->sticky);
+  return MHD_OK;
+}
+
+StageConsts make_consts(const mhd_ctx* c, double dt, double ch) {
+  StageConsts k;
+  k.gamma = c->gamma;
+  k.gm1 = c->gamma - 1.0;
+  k.igm1 = 1.0 / (c->gamma - 1.0);
+  k.p_floor = c->scheme.p_floor;
+  k.hc = 0.5 * ch;
+  k.ihc = 0.5 / ch;
+  k.ch2 = ch * ch;
+  for (int d = 0; d < 3; ++d) k.lam[d] = dt / c->dx[d];
+  k.damp = std::exp(-((c->scheme.glm_alpha * ch) * dt) / c->dxmin);  // R12
+  k.limiter = c->scheme.limiter;
+  return k;
+}
+
+// a1 (z part): fill the 2 ghost planes on each side of array U (3D only)
+int fill_z_ghosts(mhd_ctx* c, double* U) {
+  if (c->dim < 3) return MHD_OK;
+  const size_t pe = plane_elems(c), pb = pe * sizeof(double);
+  const int nz = c->nzl, g = c->gz;
+  auto P = [&](int zs) { return U + (size_t)zs * pe; };
+  const bool peri = c->bc_lo[2] == MHD_BC_PERIODIC;
+  const bool bottom_is_edge = (c->rank == 0) && !peri;
+  const bool top_is_edge = (c->rank == c->nranks - 1) && !peri;
+  if (c->nranks == 1) {
+    if (peri) {
+      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  if (bottom_is_edge) {  // outflow: U[-2] = U[-1] = U[0]
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(1), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (top_is_edge) {  // outflow: U[N] = U[N+1] = U[N-1]
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g + 1), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (c->nranks > 1) {
+    // fixed posting order on every rank (P = 2: both neighbours are the same peer; NCCL pairs
+    // sends and receives per peer in posting order)
+    NCCL_OR_RETURN(c, ncclGroupStart());
+    if (c->up >= 0) NCCL_OR_RETURN(c, ncclSend(P(nz), 2 * pe, ncclFloat64, c->up, c->comm, c->stream));
+    if (c->down >= 0) NCCL_OR_RETURN(c, ncclRecv(P(0), 2 * pe, ncclFloat64, c->down, c->comm, c->stream));
+    if (c->down >= 0) NCCL_OR_RETURN(c, ncclSend(P(g), 2 * pe, ncclFloat64, c->down, c->comm, c->stream));
+    if (c->up >= 0) NCCL_OR_RETURN(c, ncclRecv(P(nz + g), 2 * pe, ncclFloat64, c->up, c->comm, c->stream));
+    NCCL_OR_RETURN(c, ncclGroupEnd());
+  }
+  return MHD_OK;
+}
+
+// kernel timing: record a start event before a launch of class `kind`, the stop after it
+int prof_begin(mhd_ctx* c, int kind) {
+  if (!c->prof) return -1;
+  const size_t pair = c->ev_kind.size();
+  if (pair >= 4096) return -1;  // cap; read() drains
+  while (c->ev_pool.size() < 2 * (pair + 1)) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    c->ev_pool.push_back(e);
+  }
+  cudaEventRecord(c->ev_pool[2 * pair], c->stream);
+  c->ev_kind.push_back(kind);
+  return (int)pair;
+}
+void prof_end(mhd_ctx* c, int pair) {
+  if (pair >= 0) cudaEventRecord(c->ev_pool[2 * pair + 1], c->stream);
+}
+void prof_drain(mhd_ctx* c) {
+  for (size_t i = 0; i < c->ev_kind.size(); ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(c->ev_pool[2 * i + 1]);
+    cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]);
+    c->prof_ms[c->ev_kind[i]] += ms;
+    c->prof_n[c->ev_kind[i]] += 1;
+  }
+  c->ev_kind.clear();
+}
+
+int run_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+  StageArgs a;
+  a.Uin = stage == 1 ? c->U0 : c->U1;
+  a.Un = c->U0;
+  a.Uout = stage == 1 ? c->U1 : c->U0;
+  a.nx = c->nx;
+  a.ny = c->ny;
+  a.nz_loc = c->nzl;
+  a.gz = c->gz;
+  a.zoff = c->zoff;
+  a.nz_glob = c->n[2];
+  a.bcx[0] = c->bc_lo[0];
+  a.bcx[1] = c->bc_hi[0];
+  a.bcy[0] = c->bc_lo[1];
+  a.bcy[1] = c->bc_hi[1];
+  a.kz = c->kz;
+  a.stage = stage;
+  a.c = k;
+  a.counters = c->dbuf + 2;
+  a.bad = c->dbuf + 5;
+  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
+  const int pr = prof_begin(c, 0);
+  cudaError_t e = mhd::launch_stage(c->dim, c->nv, c->scheme.riemann, a, c->stream);
+  prof_end(c, pr);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "stage %d launch: %s", stage, cudaGetErrorString(e));
+  return MHD_OK;
+}
+
+// dt / c_h maxima of U^n into dbuf[0..1], reduced over ranks; reads back dbuf. Synchronising.
+int reduce_and_read(mhd_ctx* c) {
+  CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 2 * sizeof(unsigned long long), c->stream));
+  DtArgs d;
+  d.U = c->U0;
+  d.nx = c->nx;
+  d.ny = c->ny;
+  d.nz_loc = c->nzl;
+  d.gz = c->gz;
+  d.zoff = c->zoff;
+  d.gamma = c->gamma;
+  d.gm1 = c->gamma - 1.0;
+  d.p_floor = c->scheme.p_floor;
+  for (int i = 0; i < 3; ++i) d.idx[i] = 1.0 / c->dx[i];
+  d.out = c->dbuf;
+  d.bad = c->dbuf + 5;
+  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
+  const int pr = prof_begin(c, 1);
+  cudaError_t e = mhd::launch_dt(c->dim, c->nv, d, c->nsm, c->stream);
+  prof_end(c, pr);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt launch: %s", cudaGetErrorString(e));
+  unsigned long long* src = c->dbuf;
+  if (c->nranks > 1) {
+    // maxima (exact on the int64 patterns of non-negative doubles), counter sums, bad-slot minima
+    NCCL_OR_RETURN(c, ncclGroupStart());
+    NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf, c->dred, 2, ncclUint64, ncclMax, c->comm, c->stream));
+    NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf + 2, c->dred + 2, 3, ncclUint64, ncclSum, c->comm, c->stream));
+    NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf + 5, c->dred + 5, 3, ncclUint64, ncclMin, c->comm, c->stream));
+    NCCL_OR_RETURN(c, ncclGroupEnd());
+    src = c->dred;
+  }
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf, src, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  c->diag.p_floors = (int64_t)c->hbuf[2];
+  c->diag.plm_fallbacks = (int64_t)c->hbuf[3];
+  c->diag.hlld_to_hll = (int64_t)c->hbuf[4];
+  for (int s = 0; s < 3; ++s) {
+    if (c->hbuf[5 + s] != ~0ULL) {
+      c->diag.bad_stage = s;
+      c->diag.first_bad_cell = (int64_t)c->hbuf[5 + s];
+      return set_err(c, MHD_E_UNPHYSICAL, "unphysical state (stage %d, cell %lld)", s, (long long)c->hbuf[5 + s]);
+    }
+  }
+  return MHD_OK;
+}
+
+int reset_device_records(mhd_ctx* c) {
+  CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 5 * sizeof(unsigned long long), c->stream));
+  CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf + 5, 0xff, 3 * sizeof(unsigned long long), c->stream));
+  return MHD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mhd_version(void) { return kVersion; }
+
+int mhd_nccl_get_unique_id(uint8_t out[128]) {
+  if (!out) return MHD_E_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MHD_E_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return MHD_OK;
+}
+
+int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc, const mhd_scheme* scheme,
+               const mhd_dist* dist, mhd_ctx** out) {
+  if (!out) return MHD_E_ARG;
+  *out = nullptr;
+  if (!grid || !bc) return MHD_E_ARG;
+  if (!(gamma > 1.0) || !std::isfinite(gamma) || !(cfl > 0.0 && cfl < 1.0)) return MHD_E_ARG;
+  mhd_ctx* c = new (std::nothrow) mhd_ctx();
+  if (!c) return MHD_E_NOMEM;
+  c->err[0] = 0;
+  memset(&c->diag, 0, sizeof c->diag);
+  c->diag.first_bad_cell = -1;
+  c->diag.bad_stage = -1;
+  int nact = 0;
+  bool prefix = true;
+  for (int d = 0; d < 3; ++d) {
+    c->n[d] = grid->n[d];
+    c->lo[d] = grid->lo[d];
+    c->hi[d] = grid->hi[d];
+    const bool act = grid->n[d] > 1;
+    if (grid->n[d] < 1 || (act && grid->n[d] < 4) || !(grid->hi[d] > grid->lo[d]) || grid->n[d] > (1LL << 30)) {
+      delete c;
+      return MHD_E_ARG;
+    }
+    if (act && d > 0 && !(grid->n[d - 1] > 1)) prefix = false;
+    nact += act;
+    c->bc_lo[d] = bc->lo[d];
+    c->bc_hi[d] = bc->hi[d];
+    if ((bc->lo[d] != MHD_BC_PERIODIC && bc->lo[d] != MHD_BC_OUTFLOW) ||
+        (bc->hi[d] != MHD_BC_PERIODIC && bc->hi[d] != MHD_BC_OUTFLOW) ||
+        ((bc->lo[d] == MHD_BC_PERIODIC) != (bc->hi[d] == MHD_BC_PERIODIC))) {
+      delete c;
+      return MHD_E_ARG;
+    }
+    c->dx[d] = (grid->hi[d] - grid->lo[d]) / (double)grid->n[d];
+  }
+  if (nact == 0 || !prefix) {  // active axes must be x, then y, then z
+    delete c;
+    return MHD_E_ARG;
+  }
+  c->dim = nact;
+  c->dxmin = INFINITY;
+  for (int d = 0; d < c->dim; ++d) c->dxmin = c->dx[d] < c->dxmin ? c->dx[d] : c->dxmin;
+  if (scheme) {
+    c->scheme = *scheme;
+  } else {
+    c->scheme.limiter = MHD_LIM_MC;
+    c->scheme.riemann = MHD_RS_HLLD;
+    c->scheme.glm = 1;
+    c->scheme.reserved = 0;
+    c->scheme.glm_alpha = 0.1;
+    c->scheme.p_floor = 1e-12;
+  }
+  if ((c->scheme.limiter != MHD_LIM_MINMOD && c->scheme.limiter != MHD_LIM_MC) ||
+      (c->scheme.riemann != MHD_RS_HLL && c->scheme.riemann != MHD_RS_HLLD) || (c->scheme.glm != 0 && c->scheme.glm != 1) ||
+      !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm)) {
+    delete c;
+    return MHD_E_ARG;
+  }
+  c->gamma = gamma;
+  c->cfl = cfl;
+  c->nv = 8 + c->scheme.glm;
+  c->rank = dist ? dist->rank : 0;
+  c->nranks = dist ? dist->nranks : 1;
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks || (c->nranks > 1 && c->dim < 3) ||
+      (c->n[2] % c->nranks) != 0 || (c->dim == 3 && c->n[2] / c->nranks < 2)) {
+    delete c;
+    return MHD_E_ARG;
+  }
+  if (dist && dist->device >= 0) {
+    if (cudaSetDevice(dist->device) != cudaSuccess) {
+      delete c;
+      return MHD_E_CUDA;
+    }
+  }
+  cudaGetDevice(&c->device);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
+  c->nx = (int)c->n[0];
+  c->ny = (int)c->n[1];
+  c->nzl = (int)(c->n[2] / c->nranks);
+  c->zoff = (long long)c->nzl * c->rank;
+  c->gz = c->dim == 3 ? 2 : 0;
+  const bool zper = c->bc_lo[2] == MHD_BC_PERIODIC;
+  c->up = (c->nranks > 1 && (zper || c->rank < c->nranks - 1)) ? (c->rank + 1) % c->nranks : -1;
+  c->down = (c->nranks > 1 && (zper || c->rank > 0)) ? (c->rank + c->nranks - 1) % c->nranks : -1;
+  // z chunk per CTA: enough CTAs for ~4 waves of 2 CTAs/SM, at least 8 planes per chunk
+  {
+    const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + mhd::stage_tile_rows(c->dim) - 1) /
+                                                               mhd::stage_tile_rows(c->dim));
+    const long long want = (long long)c->nsm * 2 * 4;
+    long long chunks = (want + tiles - 1) / tiles;
+    if (chunks < 1) chunks = 1;
+    long long kz = (c->nzl + chunks - 1) / chunks;
+    if (kz < 8) kz = 8;
+    if (kz > c->nzl) kz = c->nzl;
+    c->kz = (int)kz;
+  }
+  c->arr_elems = plane_elems(c) * (size_t)(c->nzl + 2 * c->gz);
+  cudaError_t e1 = cudaMalloc(&c->U0, c->arr_elems * sizeof(double));
+  cudaError_t e2 = cudaMalloc(&c->U1, c->arr_elems * sizeof(double));
+  cudaError_t e3 = cudaMalloc(&c->dbuf, 24 * sizeof(unsigned long long));
+  cudaError_t e4 = cudaMallocHost(&c->hbuf, 24 * sizeof(unsigned long long));
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
+    mhd_destroy(c);
+    return MHD_E_NOMEM;
+  }
+  c->dred = c->dbuf + 8;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    mhd_destroy(c);
+    return MHD_E_CUDA;
+  }
+  c->own_stream = true;
+  // zero the arrays so ghost planes never hold garbage
+  cudaMemsetAsync(c->U0, 0, c->arr_elems * sizeof(double), c->stream);
+  cudaMemsetAsync(c->U1, 0, c->arr_elems * sizeof(double), c->stream);
+  if (reset_device_records(c) != MHD_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    mhd_destroy(c);
+    return MHD_E_CUDA;
+  }
+  if (c->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_id, sizeof id);
+    if (ncclCommInitRank(&c->comm, c->nranks, id, c->rank) != ncclSuccess) {
+      c->comm = nullptr;
+      mhd_destroy(c);
+      return MHD_E_NCCL;
+    }
+  }
+  *out = c;
+  return MHD_OK;
+}
+
+int mhd_set_stream(mhd_ctx* c, void* s) {
+  if (!c) return MHD_E_ARG;
+  if (c->own_stream && c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
+  c->stream = (cudaStream_t)s;
+  c->own_stream = false;
+  return MHD_OK;
+}
+
+int mhd_local_box(const mhd_ctx* c, int64_t off[3], int64_t ext[3]) {
+  if (!c || !off || !ext) return MHD_E_ARG;
+  off[0] = 0;
+  off[1] = 0;
+  off[2] = c->zoff;
+  ext[0] = c->nx;
+  ext[1] = c->ny;
+  ext[2] = c->nzl;
+  return MHD_OK;
+}
+
+int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
+  if (!c || !bytes) return MHD_E_ARG;
+  *bytes = 2 * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
+  return MHD_OK;
+}
+
+int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
+  if (!c || !U) return MHD_E_ARG;
+  const size_t n = plane_elems(c) * (size_t)c->nzl;
+  c->sticky = MHD_OK;
+  c->ch_valid = false;
+  c->has_state = false;
+  c->diag.first_bad_cell = -1;
+  c->diag.bad_stage = -1;
+  int rc = reset_device_records(c);
+  if (rc) return rc;
+  const double* src = U;
+  if (!on_device) {
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(c->U1, U, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    src = c->U1;
+  }
+  cudaError_t e = mhd::launch_pack(src, c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, 1, c->nsm, c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "pack: %s", cudaGetErrorString(e));
+  e = mhd::launch_validate(c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, c->zoff, c->gamma - 1.0, c->dbuf + 5, c->nsm,
+                           c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "validate: %s", cudaGetErrorString(e));
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 5, c->dbuf + 5, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                    c->stream));
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (c->hbuf[5] != ~0ULL) {
+    c->diag.bad_stage = 0;
+    c->diag.first_bad_cell = (int64_t)c->hbuf[5];
+    c->sticky = MHD_E_UNPHYSICAL;
+    CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf + 5, 0xff, sizeof(unsigned long long), c->stream));
+    return set_err(c, MHD_E_UNPHYSICAL, "set_state: unphysical cell %lld (rho<=0, p<=0 or non-finite)",
+                   (long long)c->hbuf[5]);
+  }
+  c->has_state = true;
+  return MHD_OK;
+}
+
+int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
+  if (!c || !U) return MHD_E_ARG;
+  if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  const size_t n = plane_elems(c) * (size_t)c->nzl;
+  double* dst = on_device ? U : c->U1;
+  cudaError_t e = mhd::launch_pack(c->U0, dst, c->nv, c->nx, c->ny, c->nzl, c->gz, 0, c->nsm, c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "unpack: %s", cudaGetErrorString(e));
+  if (!on_device)
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(U, c->U1, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  return MHD_OK;
+}
+
+int mhd_compute_dt(mhd_ctx* c, double* dt) {
+  if (!c || !dt) return MHD_E_ARG;
+  int rc = check_sticky(c);
+  if (rc) return rc;
+  if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  rc = reduce_and_read(c);
+  if (rc) return rc;
+  double M, S;
+  memcpy(&M, &c->hbuf[0], sizeof M);
+  memcpy(&S, &c->hbuf[1], sizeof S);
+  if (!std::isfinite(M) || !(M > 0.0)) {
+    c->diag.bad_stage = 0;
+    return set_err(c, MHD_E_UNPHYSICAL, "non-positive or non-finite signal speed maximum");
+  }
+  *dt = c->cfl / M;  // R13
+  c->ch = S;         // R11
+  c->ch_valid = true;
+  return MHD_OK;
+}
+
+int mhd_step(mhd_ctx* c, double dt) {
+  if (!c) return MHD_E_ARG;
+  int rc = check_sticky(c);
+  if (rc) return rc;
+  if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return set_err(c, MHD_E_ARG, "dt must be positive and finite");
+  if (!c->ch_valid) {
+    double tmp;
+    rc = mhd_compute_dt(c, &tmp);
+    if (rc) return rc;
+  }
+  if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
+  const StageConsts k = make_consts(c, dt, c->ch);
+  if ((rc = fill_z_ghosts(c, c->U0))) return rc;
+  if ((rc = run_stage(c, 1, k))) return rc;
+  if ((rc = fill_z_ghosts(c, c->U1))) return rc;
+  if ((rc = run_stage(c, 2, k))) return rc;
+  c->ch_valid = false;
+  c->diag.steps += 1;
+  return MHD_OK;
+}
+
+int mhd_get_diag(const mhd_ctx* c, mhd_diag* d) {
+  if (!c || !d) return MHD_E_ARG;
+  *d = c->diag;
+  return MHD_OK;
+}
+
+const char* mhd_last_error(const mhd_ctx* c) { return c ? c->err : "null context"; }
+
+void mhd_destroy(mhd_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->U0) cudaFree(c->U0);
+  if (c->U1) cudaFree(c->U1);
+  if (c->dbuf) cudaFree(c->dbuf);
+  if (c->hbuf) cudaFreeHost(c->hbuf);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
+  if (!c) return MHD_E_ARG;
+  if (c->prof) prof_drain(c);
+  c->prof = enable != 0;
+  c->prof_ms[0] = c->prof_ms[1] = 0.0;
+  c->prof_n[0] = c->prof_n[1] = 0;
+  return MHD_OK;
+}
+
+int mhd_profile_read(mhd_ctx* c, double ms[2], int64_t launches[2]) {
+  if (!c || !ms || !launches) return MHD_E_ARG;
+  prof_drain(c);
+  for (int i = 0; i < 2; ++i) {
+    ms[i] = c->prof_ms[i];
+    launches[i] = c->prof_n[i];
+  }
+  return MHD_OK;
+}
+
+int mhd_debug_face_flux(mhd_ctx* c, const double* VL, const double* VR, int64_t n, double ch, double* F,
+                        int64_t* n_hll) {
+  if (!c || !VL || !VR || !F || n < 0) return MHD_E_ARG;
+  if (n == 0) {
+    if (n_hll) *n_hll = 0;
+    return MHD_OK;
+  }
+  const StageConsts k = make_consts(c, 1.0, ch);
+  unsigned long long* cnt = c->dbuf + 16;
+  CUDA_OR_RETURN(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream));
+  cudaError_t e = mhd::launch_face_flux(c->nv, c->scheme.riemann, VL, VR, n, k, F, cnt, c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "face flux: %s", cudaGetErrorString(e));
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 16, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (n_hll) *n_hll = (int64_t)c->hbuf[16];
+  return MHD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,540 @@
+// mhd_kernels.cu — sm_100a kernels of the fp64 ideal-MHD Godunov step.
+//
+// Rows of SURVEY.md §8(a) → kernels:
+//   a1 ghost fill   : x/y periodic/outflow resolved by index wrap/clamp inside the stage
+//                     kernel (no ghost columns exist); z ghost planes (2 per side) are filled
+//                     by copies (1 GPU) or NCCL send/recv (slabs) in mhd_api.cu.
+//   a2..a5          : k_stage — one fused kernel per RK stage: cons->prim, PLM, GLM
+//                     pre-solve + HLL/HLLD face fluxes in x/y/z, flux divergence, stage
+//                     update (stage 2: RK2 average in place over U^n and psi damping).
+//   a6              : k_dt — CFL dt / c_h partial maxima (warp shuffle -> block -> int64
+//                     atomicMax on non-negative doubles, exact and order-free).
+//
+// k_stage design: a CTA owns a 32 x TY column tile and marches over a chunk
+// of z planes.  Lane = x (coalesced 256 B rows per field), warp = y row.  Shared memory
+// holds the primitive plane k with a 2-cell x/y halo (for the x and y faces), the
+// primitive plane k+1 (for the z slope of k+1), and per column the PLM state V+(k) and
+// the z-face flux F(k-1/2) carried to the next plane, plus the y-face fluxes of plane k.
+// x-face fluxes never touch shared memory: lane i computes face i-1/2 and takes face
+// i+1/2 from lane i+1 by __shfl_down_sync (lane 31 reads the tile's extra face from smem).
+// Every face is solved once per stage except the faces on tile edges in x and y (3%..5%).
+//
+// All arithmetic is the recipe of DESIGN.md §3 (see mhd_device.cuh), built with
+// --fmad=false so that results equal the CPU oracle bitwise.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "mhd_device.cuh"
+#include "mhd_kernels.h"
+
+namespace mhd {
+
+// ---------------------------------------------------------------------------------------
+// indexing helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int wrap_index(int i, int n, int bclo, int bchi) {
+  if (i < 0) return bclo == 0 ? ((i % n) + n) % n : 0;
+  if (i >= n) return bchi == 0 ? i % n : n - 1;
+  return i;
+}
+
+template <int NV>
+__device__ __forceinline__ void load_cell(const double* __restrict__ U, size_t plane_off, size_t fstride,
+                                          size_t cell, double* u) {
+#pragma unroll
+  for (int f = 0; f < NV; ++f) u[f] = __ldg(U + plane_off + f * fstride + cell);
+}
+
+// block-wide sum of three per-thread counters, one atomicAdd per counter per block
+__device__ __forceinline__ void flush_counters(int nthreads, unsigned long long* gcnt, int c0, int c1, int c2) {
+  __shared__ int red[3][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c0 += __shfl_down_sync(0xffffffffu, c0, o);
+    c1 += __shfl_down_sync(0xffffffffu, c1, o);
+    c2 += __shfl_down_sync(0xffffffffu, c2, o);
+  }
+  if (lane == 0) {
+    red[0][w] = c0;
+    red[1][w] = c1;
+    red[2][w] = c2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s0 = 0, s1 = 0, s2 = 0;
+    for (int i = 0; i < (nthreads + 31) / 32; ++i) {
+      s0 += red[0][i];
+      s1 += red[1][i];
+      s2 += red[2][i];
+    }
+    if (s0) atomicAdd(gcnt + 0, (unsigned long long)s0);
+    if (s1) atomicAdd(gcnt + 1, (unsigned long long)s1);
+    if (s2) atomicAdd(gcnt + 2, (unsigned long long)s2);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// fused stage kernel
+// ---------------------------------------------------------------------------------------
+template <int DIM, int NV, int TY>
+struct StageSmem {
+  static constexpr int TX = 32;
+  static constexpr int HY = DIM >= 2 ? 2 : 0;
+  static constexpr int PW = TX + 4;
+  static constexpr int PH = TY + 2 * HY;
+  static constexpr int nVc = NV * PH * PW;
+  static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vz1, Vpz, Fzp each
+  static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
+  static constexpr int nFxe = NV * TY;
+  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFxe);
+};
+
+template <int DIM, int NV, int RS, int TY>
+__global__ void __launch_bounds__(32 * TY, (DIM == 3) ? 2 : 1) k_stage(StageArgs a) {
+  using S = StageSmem<DIM, NV, TY>;
+  constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH;
+  constexpr int NT = 32 * TY;
+  extern __shared__ double smem[];
+  double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo)
+  double* Vz1 = Vc + S::nVc;         // [NV][TY][TX] primitives of plane k+1 (3D)
+  double* Vpz = Vz1 + S::nCol;       // [NV][TY][TX] V+ (z) of plane k        (3D)
+  double* Fzp = Vpz + S::nCol;       // [NV][TY][TX] z flux at k-1/2          (3D)
+  double* Fy = Fzp + S::nCol;        // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
+  double* Fxe = Fy + S::nFy;         // [NV][TY] flux through the tile's last x face
+
+  const StageConsts& c = a.c;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int nx = a.nx, ny = a.ny, nzl = a.nz_loc;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool own = gx < nx && gy < ny;
+  const size_t fstride = (size_t)nx * ny;
+  const size_t pstride = fstride * NV;
+  const int kb = blockIdx.z * a.kz;
+  const int ke = min(kb + a.kz, nzl);
+  int cnt_floor = 0, cnt_fb = 0, cnt_hll = 0;
+  unsigned long long badidx = ULLONG_MAX;
+
+  // own-cell offset (x, y wrapped for ragged lanes: they compute a valid duplicate and never store)
+  const int wx = wrap_index(gx, nx, a.bcx[0], a.bcx[1]);
+  const int wy = (DIM >= 2) ? wrap_index(gy, ny, a.bcy[0], a.bcy[1]) : 0;
+  const size_t own_cell = (size_t)wy * nx + wx;
+  auto plane_off = [&](int k) -> size_t { return (size_t)(k + a.gz) * pstride; };
+  auto glin = [&](int k) -> unsigned long long {
+    return ((unsigned long long)(a.zoff + k) * (unsigned long long)ny + (unsigned long long)gy) * (unsigned long long)nx +
+           (unsigned long long)gx;
+  };
+
+  // first conversion of an own interior cell: counts the floor, checks validity
+  auto convert_own = [&](int k, double* v, bool count) {
+    double u[NV];
+    load_cell<NV>(a.Uin, plane_off(k), fstride, own_cell, u);
+    const bool fl = cons2prim<NV>(u, v, c.gm1, c.p_floor);
+    if (count && own) {
+      cnt_floor += fl ? 1 : 0;
+      if (bad_state<NV>(u)) badidx = min(badidx, glin(k));
+    }
+  };
+  auto convert_any = [&](int k, int x, int y, double* v) {
+    double u[NV];
+    const int ix = wrap_index(x, nx, a.bcx[0], a.bcx[1]);
+    const int iy = (DIM >= 2) ? wrap_index(y, ny, a.bcy[0], a.bcy[1]) : 0;
+    load_cell<NV>(a.Uin, plane_off(k), fstride, (size_t)iy * nx + ix, u);
+    cons2prim<NV>(u, v, c.gm1, c.p_floor);
+  };
+  auto store_vc = [&](int r, int col, const double* v) {  // r: 0..PH-1, col: 0..PW-1
+#pragma unroll
+    for (int f = 0; f < NV; ++f) Vc[(f * PH + r) * PW + col] = v[f];
+  };
+  // halo cells of plane k into Vc: x halo of the TY rows, y halo of the TX columns
+  auto load_halo = [&](int k) {
+    constexpr int NXH = 4 * TY;
+    constexpr int NYH = (DIM >= 2) ? 4 * TX : 0;
+    for (int h = tid; h < NXH + NYH; h += NT) {
+      double v[NV];
+      if (h < NXH) {
+        const int r = h >> 2, w = h & 3;
+        const int col = (w < 2) ? w : TX + w;  // padded cols 0,1 | TX+2, TX+3
+        convert_any(k, x0 + col - 2, y0 + r, v);
+        store_vc(r + HY, col, v);
+      } else {
+        const int j = h - NXH, rs = j / TX, col = j % TX;
+        const int r = (rs < 2) ? rs : TY + rs;  // padded rows 0,1 | TY+2, TY+3
+        convert_any(k, x0 + col, y0 + r - HY, v);
+        store_vc(r, col + 2, v);
+      }
+    }
+  };
+
+  double dFz[NV];
+#pragma unroll
+  for (int f = 0; f < NV; ++f) dFz[f] = 0.0;
+
+  // ------------------------------------------------------------------ prologue
+  if constexpr (DIM == 3) {
+    double qA[NV], qB[NV], qC[NV], qD[NV], qp[NV], qm[NV], qp0[NV];
+    convert_own(kb - 2, qA, false);
+    convert_own(kb - 1, qB, false);
+    convert_own(kb, qC, true);
+    convert_own(kb + 1, qD, kb + 1 < ke);
+    plm_cell<NV>(c.limiter, qA, qB, qC, qp0, qm);          // V+(kb-1)
+    const bool fb = plm_cell<NV>(c.limiter, qB, qC, qD, qp, qm);  // V-(kb), V+(kb)
+    cnt_fb += (fb && own) ? 1 : 0;
+    double wl[NV], wr[NV], fn[NV], fz[NV];
+    to_normal<NV, 2>(qp0, wl);
+    to_normal<NV, 2>(qm, wr);
+    const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+    cnt_hll += (fell && own) ? 1 : 0;
+    from_normal<NV, 2>(fn, fz);
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+      Vpz[f * NT + tid] = qp[f];
+      Fzp[f * NT + tid] = fz[f];
+      Vz1[f * NT + tid] = qD[f];
+    }
+    store_vc(ty + HY, tx + 2, qC);
+  } else {
+    double q[NV];
+    convert_own(kb, q, true);
+    store_vc(ty + HY, tx + 2, q);
+  }
+  load_halo(kb);
+  __syncthreads();
+
+  // ------------------------------------------------------------------ march over z
+  for (int k = kb; k < ke; ++k) {
+    // ---- z face k+1/2 (3D)
+    if constexpr (DIM == 3) {
+      double q2[NV], q0[NV], q1[NV], qp[NV], qm[NV];
+      convert_own(k + 2, q2, k + 2 < ke);
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        q0[f] = Vc[(f * PH + ty + HY) * PW + tx + 2];
+        q1[f] = Vz1[f * NT + tid];
+      }
+      const bool fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);  // cell k+1
+      cnt_fb += (fb && own && k + 1 < ke) ? 1 : 0;
+      double vl[NV], wl[NV], wr[NV], fn[NV], fz[NV];
+#pragma unroll
+      for (int f = 0; f < NV; ++f) vl[f] = Vpz[f * NT + tid];
+      to_normal<NV, 2>(vl, wl);
+      to_normal<NV, 2>(qm, wr);
+      const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+      cnt_hll += (fell && own && (k + 1 < ke || a.zoff + k + 1 == a.nz_glob)) ? 1 : 0;
+      from_normal<NV, 2>(fn, fz);
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        dFz[f] = fz[f] - Fzp[f * NT + tid];
+        Fzp[f * NT + tid] = fz[f];
+        Vpz[f * NT + tid] = qp[f];
+      }
+    }
+    // ---- y faces (2D/3D): own face ty-1/2 ; extra row TY-1/2 by warp 0
+    if constexpr (DIM >= 2) {
+      auto yface = [&](int row, int col, bool count_fb, bool count_hll) {  // face between rows row-1, row
+        double qa[NV], qb[NV], qc[NV], qd[NV], qp[NV], qm[NV], tmp[NV];
+#pragma unroll
+        for (int f = 0; f < NV; ++f) {
+          const double* base = Vc + (f * PH + row + HY) * PW + col + 2;
+          qa[f] = base[-2 * PW];
+          qb[f] = base[-PW];
+          qc[f] = base[0];
+          qd[f] = base[PW];
+        }
+        plm_cell<NV>(c.limiter, qa, qb, qc, qp, tmp);             // cell row-1: V+
+        const bool fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, qm);  // cell row: V-
+        double wl[NV], wr[NV], fn[NV], fy[NV];
+        to_normal<NV, 1>(qp, wl);
+        to_normal<NV, 1>(qm, wr);
+        const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+        from_normal<NV, 1>(fn, fy);
+        cnt_fb += (fb && count_fb) ? 1 : 0;
+        cnt_hll += (fell && count_hll) ? 1 : 0;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) Fy[(f * (TY + 1) + row) * TX + col] = fy[f];
+      };
+      yface(ty, tx, own, own || (gy == ny && gx < nx));
+      if (ty == 0) {
+        const int gyl = y0 + TY;
+        yface(TY, tx, false, gyl == ny && gx < nx);
+      }
+    }
+    // ---- x faces: own face tx-1/2 in registers; extra face TX-1/2 of each row by warp 1 (or 0)
+    double fxo[NV];
+    {
+      auto xface = [&](int row, int col, double* fx) -> int {  // face between cols col-1, col
+        double qa[NV], qb[NV], qc[NV], qd[NV], qp[NV], qm[NV], tmp[NV];
+#pragma unroll
+        for (int f = 0; f < NV; ++f) {
+          const double* base = Vc + (f * PH + row + HY) * PW + col + 2;
+          qa[f] = base[-2];
+          qb[f] = base[-1];
+          qc[f] = base[0];
+          qd[f] = base[1];
+        }
+        plm_cell<NV>(c.limiter, qa, qb, qc, qp, tmp);
+        const int fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, qm) ? 1 : 0;
+        double wl[NV], wr[NV], fn[NV];
+        to_normal<NV, 0>(qp, wl);
+        to_normal<NV, 0>(qm, wr);
+        const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+        from_normal<NV, 0>(fn, fx);
+        return fb | (fell << 1);
+      };
+      const int r = xface(ty, tx, fxo);
+      cnt_fb += ((r & 1) && own) ? 1 : 0;
+      cnt_hll += ((r >> 1) && (own || (gx == nx && gy < ny))) ? 1 : 0;
+      constexpr int XW = (TY >= 2) ? 1 : 0;  // warp doing the extra x faces
+      if (ty == XW && tx < TY) {
+        double fe[NV];
+        const int re = xface(tx, TX, fe);
+        cnt_hll += ((re >> 1) && x0 + TX == nx && y0 + tx < ny) ? 1 : 0;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) Fxe[f * TY + tx] = fe[f];
+      }
+    }
+    __syncthreads();
+    // ---- update
+    {
+      double up[NV];
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        const double nb = __shfl_down_sync(0xffffffffu, fxo[f], 1);
+        up[f] = (tx == 31) ? Fxe[f * TY + ty] : nb;
+      }
+      if (own) {
+        const size_t off = plane_off(k) + (size_t)gy * nx + gx;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) {
+          double r = c.lam[0] * (up[f] - fxo[f]);
+          if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
+          if constexpr (DIM == 3) r = r + c.lam[2] * dFz[f];
+          const double s = __ldg(a.Uin + off + f * fstride) - r;  // S(U) = U - r
+          if (a.stage == 1) {
+            a.Uout[off + f * fstride] = s;
+          } else {
+            double un = a.Un[off + f * fstride];
+            double v = 0.5 * (un + s);  // U^{n+1} = (U^n + U**)/2
+            if (NV > 8 && f == NV - 1) v = v * c.damp;
+            a.Uout[off + f * fstride] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- advance the plane window (3D)
+    if constexpr (DIM == 3) {
+      if (k + 1 < ke) {
+#pragma unroll
+        for (int f = 0; f < NV; ++f) Vc[(f * PH + ty + HY) * PW + tx + 2] = Vz1[f * NT + tid];
+        load_halo(k + 1);
+        double q[NV];
+        convert_own(k + 2, q, false);
+#pragma unroll
+        for (int f = 0; f < NV; ++f) Vz1[f * NT + tid] = q[f];
+        __syncthreads();
+      }
+    }
+  }
+  if (badidx != ULLONG_MAX) atomicMin(a.bad + a.stage, badidx);
+  flush_counters(NT, a.counters, cnt_floor, cnt_fb, cnt_hll);
+}
+
+// ---------------------------------------------------------------------------------------
+// a6: dt / c_h partial maxima over the interior of U (3.12)
+// ---------------------------------------------------------------------------------------
+template <int DIM, int NV>
+__global__ void __launch_bounds__(256) k_dt(DtArgs a) {
+  const int nx = a.nx, ny = a.ny, nzl = a.nz_loc;
+  const size_t fstride = (size_t)nx * ny, pstride = fstride * NV;
+  const size_t ncell = fstride * nzl;
+  double M = 0.0, Sx = 0.0;
+  unsigned long long badidx = ULLONG_MAX;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ncell; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t k = i / fstride, cell = i % fstride;
+    double u[NV], v[NV];
+    load_cell<NV>(a.U, (k + a.gz) * pstride, fstride, cell, u);
+    if (bad_state<NV>(u)) {
+      badidx = min(badidx, (unsigned long long)((a.zoff + k) * fstride + cell));
+      continue;
+    }
+    cons2prim<NV>(u, v, a.gm1, a.p_floor);
+    double inv = 0.0, smax = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const double cf = fast_speed(a.gamma, v[0], v[4], v[5 + d], v[5 + (d + 1) % 3], v[5 + (d + 2) % 3]);
+      const double s = fabs(v[1 + d]) + cf;
+      if (d == 0) {
+        inv = s * a.idx[0];
+        smax = s;
+      } else {
+        inv = inv + s * a.idx[d];
+        smax = fmax(smax, s);
+      }
+    }
+    M = fmax(M, inv);
+    Sx = fmax(Sx, smax);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    Sx = fmax(Sx, __shfl_xor_sync(0xffffffffu, Sx, o));
+  }
+  __shared__ double red[2][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][w] = M;
+    red[1][w] = Sx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      M = fmax(M, red[0][i]);
+      Sx = fmax(Sx, red[1][i]);
+    }
+    // non-negative doubles order like their int64 bit patterns: exact, order-free max
+    atomicMax(a.out + 0, (unsigned long long)__double_as_longlong(M));
+    atomicMax(a.out + 1, (unsigned long long)__double_as_longlong(Sx));
+  }
+  if (badidx != ULLONG_MAX) atomicMin(a.bad, badidx);
+}
+
+// ---------------------------------------------------------------------------------------
+// layout conversion: ABI [f][z][y][x] (interior) <-> internal [z+gz][f][y][x]
+// ---------------------------------------------------------------------------------------
+__global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst, int nv, int nx, int ny, int nzl,
+                       int gz, int to_internal) {
+  const size_t fstride = (size_t)nx * ny;
+  const size_t n = fstride * nzl * nv;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    // i enumerates the ABI layout [f][z][cell]
+    const size_t cell = i % fstride;
+    const size_t zf = i / fstride;
+    const size_t z = zf % nzl, f = zf / nzl;
+    const size_t j = ((z + gz) * nv + f) * fstride + cell;
+    if (to_internal)
+      dst[j] = src[i];
+    else
+      dst[i] = src[j];
+  }
+}
+
+// set_state validation: rho > 0, p > 0 (before any floor), all finite
+template <int NV>
+__global__ void k_validate(const double* __restrict__ U, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
+                           unsigned long long* bad) {
+  const size_t fstride = (size_t)nx * ny, pstride = fstride * NV, ncell = fstride * nzl;
+  unsigned long long b = ULLONG_MAX;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ncell; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t k = i / fstride, cell = i % fstride;
+    double u[NV], v[NV];
+    load_cell<NV>(U, (k + gz) * pstride, fstride, cell, u);
+    bool bad = bad_state<NV>(u);
+    if (!bad) {
+      cons2prim<NV>(u, v, gm1, -1.0e300);
+      bad = !(v[4] > 0.0);
+    }
+    if (bad) b = min(b, (unsigned long long)((zoff + k) * fstride + cell));
+  }
+  if (b != ULLONG_MAX) atomicMin(bad, b);
+}
+
+// test-only face solve of independent pairs
+template <int NV, int RS>
+__global__ void k_face_flux(const double* __restrict__ VL, const double* __restrict__ VR, long long n, StageConsts c,
+                            double* __restrict__ F, unsigned long long* nhll) {
+  int cnt = 0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    double wl[NV], wr[NV], fn[NV];
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+      wl[f] = VL[q * NV + f];
+      wr[f] = VR[q * NV + f];
+    }
+    cnt += face_flux<NV, RS>(wl, wr, c, fn);
+#pragma unroll
+    for (int f = 0; f < NV; ++f) F[q * NV + f] = fn[f];
+  }
+  if (cnt) atomicAdd(nhll, (unsigned long long)cnt);
+}
+
+// ---------------------------------------------------------------------------------------
+// host-side launchers (explicit instantiations)
+// ---------------------------------------------------------------------------------------
+template <int DIM, int NV, int RS, int TY>
+static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
+  using S = StageSmem<DIM, NV, TY>;
+  auto kern = k_stage<DIM, NV, RS, TY>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.nz_loc + a.kz - 1) / a.kz);
+  kern<<<grid, 32 * TY, S::bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
+  if (dim == 3) {
+    if (riemann) return launch_stage_t<3, 9, 1, 8>(a, st);
+    return launch_stage_t<3, 9, 0, 8>(a, st);
+  }
+  if (dim == 2) {
+    if (riemann) return launch_stage_t<2, 9, 1, 8>(a, st);
+    return launch_stage_t<2, 9, 0, 8>(a, st);
+  }
+  if (nv == 9) {
+    if (riemann) return launch_stage_t<1, 9, 1, 1>(a, st);
+    return launch_stage_t<1, 9, 0, 1>(a, st);
+  }
+  if (riemann) return launch_stage_t<1, 8, 1, 1>(a, st);
+  return launch_stage_t<1, 8, 0, 1>(a, st);
+}
+
+int stage_tile_rows(int dim) { return dim >= 2 ? 8 : 1; }
+
+cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st) {
+  const size_t ncell = (size_t)a.nx * a.ny * a.nz_loc;
+  size_t blocks = (ncell + 255) / 256;
+  const size_t cap = (size_t)nsm * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (dim == 3) k_dt<3, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else if (dim == 2) k_dt<2, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else if (nv == 9) k_dt<1, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else k_dt<1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, int nzl, int gz, int to_internal,
+                        int nsm, cudaStream_t st) {
+  k_pack<<<nsm * 8, 256, 0, st>>>(src, dst, nv, nx, ny, nzl, gz, to_internal);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const double* U, int nv, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
+                            unsigned long long* bad, int nsm, cudaStream_t st) {
+  if (nv == 9) k_validate<9><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad);
+  else k_validate<8><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_face_flux(int nv, int riemann, const double* VL, const double* VR, long long n,
+                             const StageConsts& c, double* F, unsigned long long* nhll, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((n + 127) / 128 > 0 ? (n + 127) / 128 : 1);
+  if (nv == 9) {
+    if (riemann) k_face_flux<9, 1><<<blocks, 128, 0, st>>>(VL, VR, n, c, F, nhll);
+    else k_face_flux<9, 0><<<blocks, 128, 0, st>>>(VL, VR, n, c, F, nhll);
+  } else {
+    if (riemann) k_face_flux<8, 1><<<blocks, 128, 0, st>>>(VL, VR, n, c, F, nhll);
+    else k_face_flux<8, 0><<<blocks, 128, 0, st>>>(VL, VR, n, c, F, nhll);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace mhd

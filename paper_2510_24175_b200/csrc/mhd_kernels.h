@@ -1,0 +1,49 @@
+// mhd_kernels.h — internal interface between the host library (mhd_api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mhd_device.cuh"
+
+namespace mhd {
+
+// Internal state layout: [z + gz][f][y][x], x fastest, x/y unpadded (ghosts
+// resolved by index wrap/clamp), gz = 2 ghost planes per side in 3D (0 otherwise).
+struct StageArgs {
+  const double* Uin;  // stage input, read with the stencil
+  const double* Un;   // stage 2: U^n, read pointwise (aliases Uout)
+  double* Uout;       // stage 1: U*, stage 2: U^n (in place)
+  int nx, ny, nz_loc; // local interior extents
+  int gz;             // z ghost planes per side
+  long long zoff;     // global z offset of this slab
+  long long nz_glob;  // global nz
+  int bcx[2], bcy[2]; // 0 periodic, 1 outflow
+  int kz;             // z planes per CTA
+  int stage;          // 1 or 2
+  StageConsts c;
+  unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
+  unsigned long long* bad;       // [3] lowest bad global linear index per stage (0 = dt pass)
+};
+
+struct DtArgs {
+  const double* U;
+  int nx, ny, nz_loc, gz;
+  long long zoff;
+  double gamma, gm1, p_floor;
+  double idx[3];
+  unsigned long long* out;  // [2] bit patterns of max inv and max s
+  unsigned long long* bad;  // stage-0 slot
+};
+
+cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st);
+int stage_tile_rows(int dim);
+cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st);
+cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, int nzl, int gz, int to_internal,
+                        int nsm, cudaStream_t st);
+cudaError_t launch_validate(const double* U, int nv, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
+                            unsigned long long* bad, int nsm, cudaStream_t st);
+cudaError_t launch_face_flux(int nv, int riemann, const double* VL, const double* VR, long long n,
+                             const StageConsts& c, double* F, unsigned long long* nhll, cudaStream_t st);
+
+}  // namespace mhd

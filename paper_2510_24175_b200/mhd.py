@@ -1,0 +1,249 @@
+"""Thin ctypes binding of libmhd (include/mhd.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module only converts
+Python/numpy/torch arguments into the C ABI.  There is no CPU fallback: if ``libmhd.so`` is
+missing or no CUDA device is visible the calls raise.
+
+Names follow the ABI: ``create`` / ``set_state`` / ``compute_dt`` / ``step`` / ``get_state`` /
+``destroy`` (BASELINE.json north star).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import inputs as _inputs
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmhd.so")
+
+MHD_OK, MHD_E_ARG, MHD_E_STATE, MHD_E_CUDA, MHD_E_NCCL, MHD_E_NOMEM, MHD_E_UNPHYSICAL = range(7)
+_NAMES = {0: "MHD_OK", 1: "MHD_E_ARG", 2: "MHD_E_STATE", 3: "MHD_E_CUDA", 4: "MHD_E_NCCL", 5: "MHD_E_NOMEM",
+          6: "MHD_E_UNPHYSICAL"}
+
+# every symbol include/mhd.h declares (checked by the CPU test suite)
+EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_box", "mhd_device_bytes",
+           "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
+           "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version")
+
+
+class Grid(C.Structure):
+    _fields_ = [("n", C.c_int64 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3)]
+
+
+class BC(C.Structure):
+    _fields_ = [("lo", C.c_int32 * 3), ("hi", C.c_int32 * 3)]
+
+
+class Scheme(C.Structure):
+    _fields_ = [("limiter", C.c_int32), ("riemann", C.c_int32), ("glm", C.c_int32), ("reserved", C.c_int32),
+                ("glm_alpha", C.c_double), ("p_floor", C.c_double)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32),
+                ("nccl_id", C.c_uint8 * 128)]
+
+
+class Diag(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("p_floors", C.c_int64), ("plm_fallbacks", C.c_int64),
+                ("hlld_to_hll", C.c_int64), ("first_bad_cell", C.c_int64), ("bad_stage", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}
+
+
+class MhdError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libmhd.so (built in-tree by ``build.py``).  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libmhd.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    L.mhd_nccl_get_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.mhd_create.argtypes = [C.POINTER(Grid), C.c_double, C.c_double, C.POINTER(BC), C.POINTER(Scheme),
+                             C.POINTER(Dist), C.POINTER(P)]
+    L.mhd_set_stream.argtypes = [P, P]
+    L.mhd_local_box.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.mhd_device_bytes.argtypes = [P, C.POINTER(C.c_size_t)]
+    L.mhd_set_state.argtypes = [P, P, C.c_int32]
+    L.mhd_get_state.argtypes = [P, P, C.c_int32]
+    L.mhd_compute_dt.argtypes = [P, C.POINTER(C.c_double)]
+    L.mhd_step.argtypes = [P, C.c_double]
+    L.mhd_get_diag.argtypes = [P, C.POINTER(Diag)]
+    L.mhd_last_error.argtypes = [P]
+    L.mhd_last_error.restype = C.c_char_p
+    L.mhd_destroy.argtypes = [P]
+    L.mhd_destroy.restype = None
+    L.mhd_debug_face_flux.argtypes = [P, P, P, C.c_int64, C.c_double, P, C.POINTER(C.c_int64)]
+    L.mhd_version.restype = C.c_char_p
+    L.mhd_profile_enable.argtypes = [P, C.c_int32]
+    L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return load().mhd_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = load().mhd_nccl_get_unique_id(buf)
+    if rc:
+        raise MhdError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def _ptr_of(U):
+    """(pointer, on_device, nbytes) of a numpy array or a torch tensor (CPU or CUDA)."""
+    if isinstance(U, np.ndarray):
+        if U.dtype != np.float64 or not U.flags["C_CONTIGUOUS"]:
+            raise ValueError("state must be a C-contiguous float64 array")
+        return U.ctypes.data, 0, U.nbytes
+    import torch
+    if not isinstance(U, torch.Tensor):
+        raise TypeError("state must be a numpy array or a torch tensor")
+    if U.dtype != torch.float64 or not U.is_contiguous():
+        raise ValueError("state must be a contiguous float64 tensor")
+    return U.data_ptr(), 1 if U.is_cuda else 0, U.numel() * 8
+
+
+class Solver:
+    """One libmhd context: the state of this rank's slab on one GPU."""
+
+    def __init__(self, problem: "_inputs.Problem", rank: int = 0, nranks: int = 1, device: int = -1,
+                 nccl_id: Optional[bytes] = None, stream=None):
+        L = load()
+        self.problem = problem
+        g = Grid()
+        bc = BC()
+        for d in range(3):
+            g.n[d] = int(problem.n[d])
+            g.lo[d] = float(problem.lo[d])
+            g.hi[d] = float(problem.hi[d])
+            bc.lo[d] = int(problem.bc[d])
+            bc.hi[d] = int(problem.bc[d])
+        sc = Scheme(int(problem.limiter), int(problem.riemann), int(problem.glm), 0, float(problem.glm_alpha),
+                    float(problem.p_floor))
+        dist = None
+        if nranks > 1 or device >= 0:
+            dist = Dist(rank, nranks, device, 0)
+            if nccl_id is not None:
+                C.memmove(dist.nccl_id, nccl_id, 128)
+        h = C.c_void_p()
+        rc = L.mhd_create(C.byref(g), float(problem.gamma), float(problem.cfl), C.byref(bc), C.byref(sc),
+                          C.byref(dist) if dist is not None else None, C.byref(h))
+        if rc:
+            raise MhdError(rc, "mhd_create failed")
+        self._h = h
+        self._L = L
+        off, ext = (C.c_int64 * 3)(), (C.c_int64 * 3)()
+        L.mhd_local_box(h, off, ext)
+        self.offset = tuple(off)
+        self.extent = tuple(ext)
+        self.nvar = problem.nvar
+        self.local_shape = (self.nvar, ext[2], ext[1], ext[0])
+        if stream is not None:
+            self.set_stream(stream)
+
+    # --- ABI calls -------------------------------------------------------------------------
+    def _check(self, rc):
+        if rc:
+            raise MhdError(rc, self._L.mhd_last_error(self._h).decode())
+
+    def set_stream(self, stream) -> None:
+        """stream: a torch.cuda.Stream, an int handle or None (library's own stream)."""
+        handle = getattr(stream, "cuda_stream", stream)
+        self._check(self._L.mhd_set_stream(self._h, C.c_void_p(handle)))
+
+    def set_state(self, U) -> None:
+        p, dev, nbytes = _ptr_of(U)
+        if nbytes != int(np.prod(self.local_shape)) * 8:
+            raise ValueError(f"state must have shape {self.local_shape}")
+        self._check(self._L.mhd_set_state(self._h, C.c_void_p(p), dev))
+
+    def get_state(self, out=None):
+        if out is None:
+            out = np.empty(self.local_shape, dtype=np.float64)
+        p, dev, nbytes = _ptr_of(out)
+        if nbytes != int(np.prod(self.local_shape)) * 8:
+            raise ValueError(f"output must have shape {self.local_shape}")
+        self._check(self._L.mhd_get_state(self._h, C.c_void_p(p), dev))
+        return out
+
+    def compute_dt(self) -> float:
+        dt = C.c_double()
+        self._check(self._L.mhd_compute_dt(self._h, C.byref(dt)))
+        return dt.value
+
+    def step(self, dt: float) -> None:
+        self._check(self._L.mhd_step(self._h, float(dt)))
+
+    def diag(self) -> dict:
+        d = Diag()
+        self._check(self._L.mhd_get_diag(self._h, C.byref(d)))
+        return d.as_dict()
+
+    def device_bytes(self) -> int:
+        b = C.c_size_t()
+        self._check(self._L.mhd_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def debug_face_flux(self, VL, VR, ch: float):
+        """VL, VR: CUDA float64 tensors [n][nvar] (normal frame). Returns (F, n_hll)."""
+        import torch
+        F = torch.empty_like(VL)
+        nh = C.c_int64()
+        self._check(self._L.mhd_debug_face_flux(self._h, C.c_void_p(VL.data_ptr()), C.c_void_p(VR.data_ptr()),
+                                                VL.shape[0], float(ch), C.c_void_p(F.data_ptr()), C.byref(nh)))
+        return F, nh.value
+
+    def profile_enable(self, on: bool = True) -> None:
+        self._check(self._L.mhd_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        """{'stage': (ms, launches), 'dt': (ms, launches)} since profile_enable."""
+        ms, n = (C.c_double * 2)(), (C.c_int64 * 2)()
+        self._check(self._L.mhd_profile_read(self._h, ms, n))
+        return {"stage": (ms[0], n[0]), "dt": (ms[1], n[1])}
+
+    def destroy(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.mhd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # --- harness (DESIGN.md §3 c.14 driver loop) ---------------------------------------------
+    def run(self, nsteps: int, t_end: float = 0.0):
+        """compute_dt/step loop; with t_end > 0 the last dt is clamped.  Returns the dt log."""
+        log = []
+        t = 0.0
+        while len(log) < nsteps and (t_end <= 0.0 or t < t_end):
+            dt = self.compute_dt()
+            if t_end > 0.0 and t + dt > t_end:
+                dt = t_end - t
+            self.step(dt)
+            log.append(dt)
+            t = t + dt
+        return np.array(log, dtype=np.float64)

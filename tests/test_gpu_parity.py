@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI, libmhd.so) against the independent CPU oracle on
+identical seeded inputs.  Bar (BASELINE.json north star): per-field relative L-inf <= 1e-12 and an
+exactly equal dt sequence; the recipe is designed for bitwise equality, so the
+tests also report/require equal counters.  Sizes span several 32 x 8 tiles and ragged tails."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_24175_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def mhd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2510_24175_b200 import mhd as M
+    M.load()
+    return M
+
+
+def rel_linf(a, b):
+    """per-field max|a-b| / max|b| (R24)."""
+    out = []
+    for f in range(a.shape[0]):
+        scale = max(np.abs(b[f]).max(), 1e-300)
+        out.append(np.abs(a[f] - b[f]).max() / scale)
+    return np.array(out)
+
+
+def run_both(mhd, p, U0, nsteps, t_end=0.0):
+    o = oracle.Oracle(p, U0)
+    log_o = o.run(nsteps, t_end)
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    log_g = s.run(nsteps, t_end)
+    Ug = s.get_state()
+    dg = s.diag()
+    s.destroy()
+    return o, log_o, Ug, log_g, dg
+
+
+def assert_parity(o, log_o, Ug, log_g, dg, exact_counters=True):
+    assert len(log_o) == len(log_g)
+    assert np.array_equal(log_o, log_g), "dt sequences differ"
+    err = rel_linf(Ug, o.U)
+    assert np.all(err <= TOL), err
+    co = o.counters()
+    if exact_counters:
+        for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+            assert co[k] == dg[k], (k, co[k], dg[k])
+    return err
+
+
+# ---------------------------------------------------------------------------------------------
+# face solve
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("riemann", [I.HLL, I.HLLD])
+@pytest.mark.parametrize("glm", [0, 1])
+@pytest.mark.parametrize("jump", [None, 0.5, 0.05])
+def test_face_flux_bitwise(mhd, riemann, glm, jump):
+    import torch
+    p = I.Problem("ff", (8, 1, 1), riemann=riemann, glm=glm)
+    VL, VR = I.random_face_states(20000, seed=101 + (0 if jump is None else int(jump * 100)), glm=bool(glm),
+                                  jump=jump)
+    if not glm:
+        VR[:, 5] = VL[:, 5]
+    ch = 3.3
+    Fo, nfo = oracle.face_flux(p, VL, VR, ch)
+    s = mhd.Solver(p)
+    Fg, nfg = s.debug_face_flux(torch.from_numpy(VL).cuda(), torch.from_numpy(VR).cuda(), ch)
+    s.destroy()
+    Fg = Fg.cpu().numpy()
+    assert nfo == nfg
+    assert np.array_equal(Fo, Fg), np.abs(Fo - Fg).max()
+
+
+# ---------------------------------------------------------------------------------------------
+# whole runs
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("riemann,limiter", [(I.HLL, I.MC), (I.HLLD, I.MC), (I.HLL, I.MINMOD)])
+def test_brio_wu_full_run(mhd, riemann, limiter):
+    """BASELINE configs[0]: Brio-Wu 512, PLM+HLL, RK2, CFL 0.4, to t = 0.1 (full run)."""
+    p = I.brio_wu(512, riemann=riemann, limiter=limiter)
+    res = run_both(mhd, p, I.brio_wu_ic(p), 100000, p.t_end)
+    assert_parity(*res)
+    assert 480 < len(res[1]) < 500
+
+
+def test_sod_outflow(mhd):
+    p = I.sod(300)
+    assert_parity(*run_both(mhd, p, I.sod_ic(p), 100000, p.t_end))
+
+
+def test_1d_glm(mhd):
+    p = I.brio_wu(200).replace(glm=1)
+    assert_parity(*run_both(mhd, p, I.brio_wu_ic(p), 150))
+
+
+@pytest.mark.parametrize("n", [(64, 64), (50, 37)])
+def test_ot2d(mhd, n):
+    p = I.orszag_tang_2d(64).replace(n=(n[0], n[1], 1))
+    assert_parity(*run_both(mhd, p, I.orszag_tang_2d_ic(p), 120))
+
+
+@pytest.mark.parametrize("limiter,riemann", [(I.MC, I.HLLD), (I.MINMOD, I.HLLD), (I.MC, I.HLL)])
+def test_ot3d_small(mhd, limiter, riemann):
+    p = I.orszag_tang_3d(32, limiter=limiter, riemann=riemann)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    assert_parity(*run_both(mhd, p, U0, 15))
+
+
+def test_ot3d_ragged(mhd):
+    """ragged tiles in x (40 = 32 + 8) and y (21 = 2*8 + 5) and a z extent that is not a chunk multiple."""
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 19), hi=(1.25, 0.65625, 0.59375))
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    assert_parity(*run_both(mhd, p, U0, 10))
+
+
+def test_blast3d_small(mhd):
+    p = I.blast_3d(32)
+    assert_parity(*run_both(mhd, p, I.blast_3d_ic(p), 20))
+
+
+def test_3d_outflow_shock_tube_along_z(mhd):
+    """Brio-Wu along z inside a 3D box with outflow on every face: exercises the z outflow ghost
+    planes and the z frame (z, x, y) of the face solve."""
+    n = 48
+    p = I.Problem("bwz", (8, 8, n), bc=(I.OUTFLOW,) * 3, gamma=2.0, glm=1, riemann=I.HLLD)
+    pz = I.brio_wu(n).replace(glm=1)
+    U1 = I.brio_wu_ic(pz)[:, 0, 0, :]  # [nv][n] along x
+    U = np.zeros(p.shape)
+    for f in range(9):
+        src = f
+        if 1 <= f <= 3:
+            src = 1 + (f - 1 - 2) % 3
+        if 5 <= f <= 7:
+            src = 5 + (f - 5 - 2) % 3
+        U[f] = U1[src][:, None, None]
+    assert_parity(*run_both(mhd, p, U, 40))
+
+
+# ---------------------------------------------------------------------------------------------
+# API behaviour
+# ---------------------------------------------------------------------------------------------
+def test_state_roundtrip_host_and_device(mhd):
+    import torch
+    p = I.orszag_tang_3d(16)
+    U = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U)
+    assert np.array_equal(s.get_state(), U)
+    Ud = torch.from_numpy(U).cuda()
+    s.set_state(Ud)
+    out = torch.empty_like(Ud)
+    s.get_state(out)
+    assert torch.equal(out, Ud)
+    s.destroy()
+
+
+def test_unphysical_state_rejected_and_sticky(mhd):
+    p = I.orszag_tang_3d(16)
+    U = I.orszag_tang_3d_ic(p)
+    good = U[0, 3, 2, 5]
+    U[0, 3, 2, 5] = -1.0
+    s = mhd.Solver(p)
+    with pytest.raises(mhd.MhdError) as e:
+        s.set_state(U)
+    assert e.value.code == mhd.MHD_E_UNPHYSICAL
+    d = s.diag()
+    assert d["first_bad_cell"] == (3 * 16 + 2) * 16 + 5 and d["bad_stage"] == 0
+    with pytest.raises(mhd.MhdError) as e:
+        s.compute_dt()
+    assert e.value.code == mhd.MHD_E_STATE
+    U[0, 3, 2, 5] = good
+    s.set_state(U)           # recovers
+    assert s.compute_dt() > 0
+    s.destroy()
+
+
+def test_step_unphysical_detected(mhd):
+    """an extreme rarefaction with a CFL near 1 drives rho negative inside a step; the library
+    reports MHD_E_UNPHYSICAL at the next synchronising call, like the oracle."""
+    p = I.Problem("vac", (64, 1, 1), bc=(I.OUTFLOW,) * 3, gamma=1.4, glm=0, riemann=I.HLL, cfl=0.95,
+                  p_floor=1e-12)
+    X = I.centres(p, 0)
+    U = I.prim_to_cons_ic(p, 1e-6 + 0 * X, np.where(X < 0.5, -50.0, 50.0), 0, 0, 1e-8, 0, 0, 0)
+    o = oracle.Oracle(p, U)
+    s = mhd.Solver(p)
+    s.set_state(U)
+    raised_o = raised_g = None
+    try:
+        o.run(50)
+    except oracle.OracleError as e:
+        raised_o = e.counters.as_dict()
+    try:
+        s.run(50)
+    except mhd.MhdError as e:
+        raised_g = s.diag()
+        assert e.code == mhd.MHD_E_UNPHYSICAL
+    s.destroy()
+    if raised_o is None:
+        assert raised_g is None
+    else:
+        assert raised_g is not None
+        assert raised_g["first_bad_cell"] == raised_o["first_bad_cell"]
+        assert raised_g["bad_stage"] == raised_o["bad_stage"]
+
+
+def test_invalid_arguments(mhd):
+    with pytest.raises(mhd.MhdError) as e:
+        mhd.Solver(I.orszag_tang_3d(16).replace(cfl=1.5))
+    assert e.value.code == mhd.MHD_E_ARG
+    with pytest.raises(mhd.MhdError):
+        mhd.Solver(I.orszag_tang_2d(16, glm=0))  # GLM required in multi-D
+    s = mhd.Solver(I.orszag_tang_3d(16))
+    with pytest.raises(mhd.MhdError) as e:
+        s.compute_dt()                              # no state yet
+    assert e.value.code == mhd.MHD_E_STATE
+    s.destroy()
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE full size (configs[2], 256^3) in the bench's launch configuration
+# ---------------------------------------------------------------------------------------------
+def test_ot3d_256_full_size_parity(mhd):
+    """two full steps of the 256^3 OT-3D roofline config, element by element (the oracle runs
+    multi-threaded on the host; it finishes in seconds)."""
+    p = I.orszag_tang_3d(256)
+    U0 = I.orszag_tang_3d_ic(p)
+    res = run_both(mhd, p, U0, 2)
+    assert_parity(*res)
