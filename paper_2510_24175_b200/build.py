@@ -35,13 +35,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """defines: extra -D macros (tile-shape variants for A/B measurements, e.g. MHD_TY3=4)."""
+    global OUT
+    if out is not None:
+        OUT_, OUT = OUT, out
+        try:
+            return build(force=True, verbose=verbose, defines=defines)
+        finally:
+            OUT = OUT_
     if not force and not needs_build():
         return OUT
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-           "-shared", "-I", os.path.join(ROOT, "include"), "-I", inc,
+           "-shared", "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines],
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", OUT + ".tmp"]
     if verbose:
@@ -53,4 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else None,
+                defines=defs))

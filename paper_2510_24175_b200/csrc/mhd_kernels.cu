@@ -86,24 +86,38 @@ struct StageSmem {
   static constexpr int PW = TX + 4;
   static constexpr int PH = TY + 2 * HY;
   static constexpr int nVc = NV * PH * PW;
-  static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vz1, Vpz, Fzp each
+  static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vpz, Fz[0], Fz[1] each
   static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
-  static constexpr int nFxe = NV * TY;
-  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFxe);
+  static constexpr int nFx = NV * TY * (TX + 1);
+  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx);
 };
 
+template <int TY>
+struct StageOcc {
+  static constexpr int value = TY <= 4 ? 3 : (TY <= 6 ? 2 : 1);
+};
+
+// One CTA: a 32 x TY column tile, z chunk [kb, ke).  Per plane k every thread runs a short
+// loop of "face jobs" that all go through ONE inlined face solve (I-cache: the HLLD solve is
+// ~18 KB of SASS; instantiating it once keeps the kernel resident in the instruction cache):
+//   job 0 (3D)  z face k+1/2 of the thread's column   (VL = V+(k) carried in smem)
+//   job 1 (2D+) y face of the thread's cell (row ty - 1/2)
+//   job 2       tile-edge faces: warp 0 the y faces of row TY - 1/2, warp 1 the x faces of
+//               column TX - 1/2 (one per row); other warps skip
+//   job 3       x face of the thread's cell (column tx - 1/2)
+// Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
+// r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
 template <int DIM, int NV, int RS, int TY>
-__global__ void __launch_bounds__(32 * TY, (DIM == 3) ? 2 : 1) k_stage(StageArgs a) {
+__global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArgs a) {
   using S = StageSmem<DIM, NV, TY>;
   constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH;
   constexpr int NT = 32 * TY;
   extern __shared__ double smem[];
   double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo)
-  double* Vz1 = Vc + S::nVc;         // [NV][TY][TX] primitives of plane k+1 (3D)
-  double* Vpz = Vz1 + S::nCol;       // [NV][TY][TX] V+ (z) of plane k        (3D)
-  double* Fzp = Vpz + S::nCol;       // [NV][TY][TX] z flux at k-1/2          (3D)
-  double* Fy = Fzp + S::nCol;        // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
-  double* Fxe = Fy + S::nFy;         // [NV][TY] flux through the tile's last x face
+  double* Vpz = Vc + S::nVc;         // [NV][TY][TX] V+ (z) of plane k        (3D)
+  double* Fz = Vpz + S::nCol;        // [2][NV][TY][TX] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
+  double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
+  double* Fx = Fy + S::nFy;          // [NV][TY][TX+1] x-face fluxes of plane k
 
   const StageConsts& c = a.c;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -127,8 +141,8 @@ __global__ void __launch_bounds__(32 * TY, (DIM == 3) ? 2 : 1) k_stage(StageArgs
     return ((unsigned long long)(a.zoff + k) * (unsigned long long)ny + (unsigned long long)gy) * (unsigned long long)nx +
            (unsigned long long)gx;
   };
-
-  // first conversion of an own interior cell: counts the floor, checks validity
+  // conversion of the thread's own cell of plane k; `count` marks the one conversion per
+  // (interior cell, stage) that counts floors and checks validity
   auto convert_own = [&](int k, double* v, bool count) {
     double u[NV];
     load_cell<NV>(a.Uin, plane_off(k), fstride, own_cell, u);
@@ -149,8 +163,13 @@ __global__ void __launch_bounds__(32 * TY, (DIM == 3) ? 2 : 1) k_stage(StageArgs
 #pragma unroll
     for (int f = 0; f < NV; ++f) Vc[(f * PH + r) * PW + col] = v[f];
   };
-  // halo cells of plane k into Vc: x halo of the TY rows, y halo of the TX columns
-  auto load_halo = [&](int k) {
+  // plane k into Vc: interior (own cell) + x halo of the TY rows + y halo of the TX columns
+  auto load_plane = [&](int k, bool count_own) {
+    {
+      double v[NV];
+      convert_own(k, v, count_own);
+      store_vc(ty + HY, tx + 2, v);
+    }
     constexpr int NXH = 4 * TY;
     constexpr int NYH = (DIM >= 2) ? 4 * TX : 0;
     for (int h = tid; h < NXH + NYH; h += NT) {
@@ -169,172 +188,161 @@ __global__ void __launch_bounds__(32 * TY, (DIM == 3) ? 2 : 1) k_stage(StageArgs
     }
   };
 
-  double dFz[NV];
-#pragma unroll
-  for (int f = 0; f < NV; ++f) dFz[f] = 0.0;
-
   // ------------------------------------------------------------------ prologue
+  int kstart = kb;
   if constexpr (DIM == 3) {
-    double qA[NV], qB[NV], qC[NV], qD[NV], qp[NV], qm[NV], qp0[NV];
+    // V+(kb-1) into Vpz; V(kb-1) as the centre of Vc (read by the z job of iteration kb-1)
+    double qA[NV], qB[NV], qC[NV], qp[NV], qm[NV];
     convert_own(kb - 2, qA, false);
     convert_own(kb - 1, qB, false);
-    convert_own(kb, qC, true);
-    convert_own(kb + 1, qD, kb + 1 < ke);
-    plm_cell<NV>(c.limiter, qA, qB, qC, qp0, qm);          // V+(kb-1)
-    const bool fb = plm_cell<NV>(c.limiter, qB, qC, qD, qp, qm);  // V-(kb), V+(kb)
-    cnt_fb += (fb && own) ? 1 : 0;
-    double wl[NV], wr[NV], fn[NV], fz[NV];
-    to_normal<NV, 2>(qp0, wl);
-    to_normal<NV, 2>(qm, wr);
-    const int fell = face_flux<NV, RS>(wl, wr, c, fn);
-    cnt_hll += (fell && own) ? 1 : 0;
-    from_normal<NV, 2>(fn, fz);
+    convert_own(kb, qC, true);  // the counted conversion of plane kb
+    plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
+    double wp[NV];
+    to_normal<NV, 2>(qp, wp);  // Vpz is kept in the z normal frame
 #pragma unroll
-    for (int f = 0; f < NV; ++f) {
-      Vpz[f * NT + tid] = qp[f];
-      Fzp[f * NT + tid] = fz[f];
-      Vz1[f * NT + tid] = qD[f];
-    }
-    store_vc(ty + HY, tx + 2, qC);
+    for (int f = 0; f < NV; ++f) Vpz[f * NT + tid] = wp[f];
+    store_vc(ty + HY, tx + 2, qB);
+    kstart = kb - 1;
+    __syncthreads();
   } else {
-    double q[NV];
-    convert_own(kb, q, true);
-    store_vc(ty + HY, tx + 2, q);
+    load_plane(kb, true);
+    __syncthreads();
   }
-  load_halo(kb);
-  __syncthreads();
 
   // ------------------------------------------------------------------ march over z
-  for (int k = kb; k < ke; ++k) {
-    // ---- z face k+1/2 (3D)
-    if constexpr (DIM == 3) {
-      double q2[NV], q0[NV], q1[NV], qp[NV], qm[NV];
-      convert_own(k + 2, q2, k + 2 < ke);
-#pragma unroll
-      for (int f = 0; f < NV; ++f) {
-        q0[f] = Vc[(f * PH + ty + HY) * PW + tx + 2];
-        q1[f] = Vz1[f * NT + tid];
-      }
-      const bool fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);  // cell k+1
-      cnt_fb += (fb && own && k + 1 < ke) ? 1 : 0;
-      double vl[NV], wl[NV], wr[NV], fn[NV], fz[NV];
-#pragma unroll
-      for (int f = 0; f < NV; ++f) vl[f] = Vpz[f * NT + tid];
-      to_normal<NV, 2>(vl, wl);
-      to_normal<NV, 2>(qm, wr);
-      const int fell = face_flux<NV, RS>(wl, wr, c, fn);
-      cnt_hll += (fell && own && (k + 1 < ke || a.zoff + k + 1 == a.nz_glob)) ? 1 : 0;
-      from_normal<NV, 2>(fn, fz);
-#pragma unroll
-      for (int f = 0; f < NV; ++f) {
-        dFz[f] = fz[f] - Fzp[f * NT + tid];
-        Fzp[f * NT + tid] = fz[f];
-        Vpz[f * NT + tid] = qp[f];
-      }
-    }
-    // ---- y faces (2D/3D): own face ty-1/2 ; extra row TY-1/2 by warp 0
-    if constexpr (DIM >= 2) {
-      auto yface = [&](int row, int col, bool count_fb, bool count_hll) {  // face between rows row-1, row
-        double qa[NV], qb[NV], qc[NV], qd[NV], qp[NV], qm[NV], tmp[NV];
-#pragma unroll
-        for (int f = 0; f < NV; ++f) {
-          const double* base = Vc + (f * PH + row + HY) * PW + col + 2;
-          qa[f] = base[-2 * PW];
-          qb[f] = base[-PW];
-          qc[f] = base[0];
-          qd[f] = base[PW];
+  for (int k = kstart; k < ke; ++k) {
+    const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
+    const int jfirst = (DIM == 3) ? 0 : 1;
+    const int jlast = full ? 3 : 0;
+#pragma unroll 1
+    for (int job = jfirst; job <= jlast; ++job) {
+      // ---- select the face of this job
+      int d = 0, row = ty, col = tx;
+      bool active = true, cnt_right = false, cnt_face = false;
+      if (job == 0) {
+        d = 2;
+        cnt_right = own && k + 1 < ke;
+        cnt_face = own && (k + 1 < ke || a.zoff + k + 1 == a.nz_glob);
+      } else if (job == 1) {
+        d = 1;
+        active = DIM >= 2;
+        cnt_right = own;
+        cnt_face = own || (gy == ny && gx < nx);
+      } else if (job == 2) {
+        if (DIM >= 2 && ty == 0) {  // y faces of row TY - 1/2
+          d = 1;
+          row = TY;
+          cnt_face = (y0 + TY == ny) && gx < nx;
+        } else if (ty == ((DIM >= 2 && TY >= 2) ? 1 : 0) && tx < TY) {  // x faces of column TX - 1/2
+          d = 0;
+          row = tx;
+          col = TX;
+          cnt_face = (x0 + TX == nx) && (y0 + tx < ny);
+        } else {
+          active = false;
         }
-        plm_cell<NV>(c.limiter, qa, qb, qc, qp, tmp);             // cell row-1: V+
-        const bool fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, qm);  // cell row: V-
-        double wl[NV], wr[NV], fn[NV], fy[NV];
-        to_normal<NV, 1>(qp, wl);
-        to_normal<NV, 1>(qm, wr);
-        const int fell = face_flux<NV, RS>(wl, wr, c, fn);
-        from_normal<NV, 1>(fn, fy);
-        cnt_fb += (fb && count_fb) ? 1 : 0;
-        cnt_hll += (fell && count_hll) ? 1 : 0;
-#pragma unroll
-        for (int f = 0; f < NV; ++f) Fy[(f * (TY + 1) + row) * TX + col] = fy[f];
-      };
-      yface(ty, tx, own, own || (gy == ny && gx < nx));
-      if (ty == 0) {
-        const int gyl = y0 + TY;
-        yface(TY, tx, false, gyl == ny && gx < nx);
+      } else {
+        d = 0;
+        cnt_right = own;
+        cnt_face = own || (gx == nx && gy < ny);
       }
-    }
-    // ---- x faces: own face tx-1/2 in registers; extra face TX-1/2 of each row by warp 1 (or 0)
-    double fxo[NV];
-    {
-      auto xface = [&](int row, int col, double* fx) -> int {  // face between cols col-1, col
-        double qa[NV], qb[NV], qc[NV], qd[NV], qp[NV], qm[NV], tmp[NV];
+      if (!active) continue;  // warp-uniform
+      // ---- gather the two face states (normal frame) with PLM
+      // x/y jobs read Vc with the frame permutation folded into the field addresses
+      // (component n of the normal frame of direction d is field fo[n]); PLM is
+      // component-wise, so reconstructing in the normal frame is value-identical.
+      int fo[NV];
 #pragma unroll
-        for (int f = 0; f < NV; ++f) {
-          const double* base = Vc + (f * PH + row + HY) * PW + col + 2;
-          qa[f] = base[-2];
-          qb[f] = base[-1];
-          qc[f] = base[0];
-          qd[f] = base[1];
-        }
-        plm_cell<NV>(c.limiter, qa, qb, qc, qp, tmp);
-        const int fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, qm) ? 1 : 0;
-        double wl[NV], wr[NV], fn[NV];
-        to_normal<NV, 0>(qp, wl);
-        to_normal<NV, 0>(qm, wr);
-        const int fell = face_flux<NV, RS>(wl, wr, c, fn);
-        from_normal<NV, 0>(fn, fx);
-        return fb | (fell << 1);
-      };
-      const int r = xface(ty, tx, fxo);
-      cnt_fb += ((r & 1) && own) ? 1 : 0;
-      cnt_hll += ((r >> 1) && (own || (gx == nx && gy < ny))) ? 1 : 0;
-      constexpr int XW = (TY >= 2) ? 1 : 0;  // warp doing the extra x faces
-      if (ty == XW && tx < TY) {
-        double fe[NV];
-        const int re = xface(tx, TX, fe);
-        cnt_hll += ((re >> 1) && x0 + TX == nx && y0 + tx < ny) ? 1 : 0;
-#pragma unroll
-        for (int f = 0; f < NV; ++f) Fxe[f * TY + tx] = fe[f];
+      for (int n = 0; n < NV; ++n) fo[n] = n;
+      if (d == 1) {
+        fo[1] = 2; fo[2] = 3; fo[3] = 1; fo[5] = 6; fo[6] = 7; fo[7] = 5;
       }
-    }
-    __syncthreads();
-    // ---- update
-    {
-      double up[NV];
+      double wl[NV], wr[NV];
+      {
+        bool fb;
+        if (job == 0) {
+          double q0[NV], q1[NV], q2[NV], qp[NV], qm[NV];
 #pragma unroll
-      for (int f = 0; f < NV; ++f) {
-        const double nb = __shfl_down_sync(0xffffffffu, fxo[f], 1);
-        up[f] = (tx == 31) ? Fxe[f * TY + ty] : nb;
-      }
-      if (own) {
-        const size_t off = plane_off(k) + (size_t)gy * nx + gx;
-#pragma unroll
-        for (int f = 0; f < NV; ++f) {
-          double r = c.lam[0] * (up[f] - fxo[f]);
-          if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
-          if constexpr (DIM == 3) r = r + c.lam[2] * dFz[f];
-          const double s = __ldg(a.Uin + off + f * fstride) - r;  // S(U) = U - r
-          if (a.stage == 1) {
-            a.Uout[off + f * fstride] = s;
-          } else {
-            double un = a.Un[off + f * fstride];
-            double v = 0.5 * (un + s);  // U^{n+1} = (U^n + U**)/2
-            if (NV > 8 && f == NV - 1) v = v * c.damp;
-            a.Uout[off + f * fstride] = v;
+          for (int f = 0; f < NV; ++f) {
+            q0[f] = Vc[(f * PH + ty + HY) * PW + tx + 2];
+            wl[f] = Vpz[f * NT + tid];
           }
+          convert_own(k + 1, q1, false);
+          convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
+          fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);  // cell k+1
+          double wp[NV];
+          to_normal<NV, 2>(qp, wp);
+          to_normal<NV, 2>(qm, wr);
+#pragma unroll
+          for (int f = 0; f < NV; ++f) Vpz[f * NT + tid] = wp[f];
+        } else {
+          const int s = (d == 0) ? 1 : PW;
+          double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
+#pragma unroll
+          for (int n = 0; n < NV; ++n) {
+            const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + 2;
+            qa[n] = base[-2 * s];
+            qb[n] = base[-s];
+            qc[n] = base[0];
+            qd[n] = base[s];
+          }
+          plm_cell<NV>(c.limiter, qa, qb, qc, wl, tmp);       // left cell: V+
+          fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, wr);  // right cell: V-
+        }
+        cnt_fb += (fb && cnt_right) ? 1 : 0;
+      }
+      // ---- the face solve (single instance)
+      double fn[NV];
+      const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+      cnt_hll += (fell && cnt_face) ? 1 : 0;
+      // ---- scatter (back to x,y,z components through the same field map)
+      if (job == 0) {
+        double fz[NV];
+        from_normal<NV, 2>(fn, fz);
+        double* dst = Fz + ((k + 1) & 1) * S::nCol;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) dst[f * NT + tid] = fz[f];
+      } else if (d == 1) {
+#pragma unroll
+        for (int n = 0; n < NV; ++n) Fy[(fo[n] * (TY + 1) + row) * TX + col] = fn[n];
+      } else {
+#pragma unroll
+        for (int n = 0; n < NV; ++n) Fx[(n * TY + row) * (TX + 1) + col] = fn[n];
+      }
+    }
+    if (!full) {  // 3D prologue iteration: bring plane kb into Vc
+      __syncthreads();
+      load_plane(kb, false);
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz)
+    if (own) {
+      const size_t off = plane_off(k) + (size_t)gy * nx + gx;
+      const double* fzn = Fz + ((k + 1) & 1) * S::nCol;
+      const double* fzo = Fz + (k & 1) * S::nCol;
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        double r = c.lam[0] * (Fx[(f * TY + ty) * (TX + 1) + tx + 1] - Fx[(f * TY + ty) * (TX + 1) + tx]);
+        if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
+        if constexpr (DIM == 3) r = r + c.lam[2] * (fzn[f * NT + tid] - fzo[f * NT + tid]);
+        const double s = __ldg(a.Uin + off + f * fstride) - r;
+        if (a.stage == 1) {
+          a.Uout[off + f * fstride] = s;
+        } else {
+          const double un = a.Un[off + f * fstride];
+          double v = 0.5 * (un + s);  // U^{n+1} = (U^n + U**)/2
+          if (NV > 8 && f == NV - 1) v = v * c.damp;
+          a.Uout[off + f * fstride] = v;
         }
       }
     }
-    __syncthreads();
     // ---- advance the plane window (3D)
     if constexpr (DIM == 3) {
       if (k + 1 < ke) {
-#pragma unroll
-        for (int f = 0; f < NV; ++f) Vc[(f * PH + ty + HY) * PW + tx + 2] = Vz1[f * NT + tid];
-        load_halo(k + 1);
-        double q[NV];
-        convert_own(k + 2, q, false);
-#pragma unroll
-        for (int f = 0; f < NV; ++f) Vz1[f * NT + tid] = q[f];
+        __syncthreads();
+        load_plane(k + 1, false);
         __syncthreads();
       }
     }
@@ -479,14 +487,20 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+#ifndef MHD_TY3
+#define MHD_TY3 6
+#endif
+#ifndef MHD_TY2
+#define MHD_TY2 8
+#endif
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
   if (dim == 3) {
-    if (riemann) return launch_stage_t<3, 9, 1, 8>(a, st);
-    return launch_stage_t<3, 9, 0, 8>(a, st);
+    if (riemann) return launch_stage_t<3, 9, 1, MHD_TY3>(a, st);
+    return launch_stage_t<3, 9, 0, MHD_TY3>(a, st);
   }
   if (dim == 2) {
-    if (riemann) return launch_stage_t<2, 9, 1, 8>(a, st);
-    return launch_stage_t<2, 9, 0, 8>(a, st);
+    if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2>(a, st);
+    return launch_stage_t<2, 9, 0, MHD_TY2>(a, st);
   }
   if (nv == 9) {
     if (riemann) return launch_stage_t<1, 9, 1, 1>(a, st);
@@ -496,7 +510,7 @@ cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaS
   return launch_stage_t<1, 8, 0, 1>(a, st);
 }
 
-int stage_tile_rows(int dim) { return dim >= 2 ? 8 : 1; }
+int stage_tile_rows(int dim) { return dim == 3 ? MHD_TY3 : (dim == 2 ? MHD_TY2 : 1); }
 
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st) {
   const size_t ncell = (size_t)a.nx * a.ny * a.nz_loc;

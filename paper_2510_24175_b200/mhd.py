@@ -18,7 +18,7 @@ import numpy as np
 from . import inputs as _inputs
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmhd.so")
+LIB_PATH = os.environ.get("MHD_LIB") or os.path.join(_HERE, "libmhd.so")  # MHD_LIB: A/B builds
 
 MHD_OK, MHD_E_ARG, MHD_E_STATE, MHD_E_CUDA, MHD_E_NCCL, MHD_E_NOMEM, MHD_E_UNPHYSICAL = range(7)
 _NAMES = {0: "MHD_OK", 1: "MHD_E_ARG", 2: "MHD_E_STATE", 3: "MHD_E_CUDA", 4: "MHD_E_NCCL", 5: "MHD_E_NOMEM",
