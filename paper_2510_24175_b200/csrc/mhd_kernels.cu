@@ -47,6 +47,9 @@ __device__ __forceinline__ void load_cell(const double* __restrict__ U, size_t p
   for (int f = 0; f < NV; ++f) u[f] = __ldg(U + plane_off + f * fstride + cell);
 }
 
+__device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // block-wide sum of three per-thread counters, one atomicAdd per counter per block
 __device__ __forceinline__ void flush_counters(int nthreads, unsigned long long* gcnt, int c0, int c1, int c2) {
   __shared__ int red[3][32];
@@ -212,6 +215,15 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
   // ------------------------------------------------------------------ march over z
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
+    if constexpr (DIM == 3) {
+      // latency hiding: the own column of plane k+3 (first touched next iteration) into L2,
+      // and the own cell of plane k (re-read by the update at the end of this iteration) into L1
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        prefetch_l2(a.Uin + plane_off(k + 3 < nzl + a.gz ? k + 3 : k) + f * fstride + own_cell);
+        if (full) prefetch_l1(a.Uin + plane_off(k) + f * fstride + own_cell);
+      }
+    }
     const int jfirst = (DIM == 3) ? 0 : 1;
     const int jlast = full ? 3 : 0;
 #pragma unroll 1
