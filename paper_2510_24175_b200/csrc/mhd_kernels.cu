@@ -81,6 +81,9 @@ __device__ __forceinline__ void flush_counters(int nthreads, unsigned long long*
 
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
+#ifndef MHD_OCC3
+#define MHD_OCC3 2
+#endif
 // ---------------------------------------------------------------------------------------
 template <int DIM, int NV, int TY>
 struct StageSmem {
@@ -88,6 +91,7 @@ struct StageSmem {
   static constexpr int HY = DIM >= 2 ? 2 : 0;
   static constexpr int PW = TX + 4;
   static constexpr int PH = TY + 2 * HY;
+  static constexpr int NT = 32 * (TY + 1);  // TY cell warps + 1 edge warp
   static constexpr int nVc = NV * PH * PW;
   static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vpz, Fz[0], Fz[1] each
   static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
@@ -95,39 +99,42 @@ struct StageSmem {
   static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx);
 };
 
-template <int TY>
+template <int DIM, int TY>
 struct StageOcc {
-  static constexpr int value = TY <= 4 ? 3 : (TY <= 6 ? 2 : 1);
+  static constexpr int value = DIM == 3 ? MHD_OCC3 : (DIM == 2 ? 2 : 4);
 };
 
-// One CTA: a 32 x TY column tile, z chunk [kb, ke).  Per plane k every thread runs a short
-// loop of "face jobs" that all go through ONE inlined face solve (I-cache: the HLLD solve is
-// ~18 KB of SASS; instantiating it once keeps the kernel resident in the instruction cache):
-//   job 0 (3D)  z face k+1/2 of the thread's column   (VL = V+(k) carried in smem)
-//   job 1 (2D+) y face of the thread's cell (row ty - 1/2)
-//   job 2       tile-edge faces: warp 0 the y faces of row TY - 1/2, warp 1 the x faces of
-//               column TX - 1/2 (one per row); other warps skip
-//   job 3       x face of the thread's cell (column tx - 1/2)
-// Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
+// One CTA: a 32 x TY cell tile (TY "cell warps", lane = x) plus one "edge warp", marching
+// over the z chunk [kb, ke).  Per plane k each warp runs a short loop of face jobs that all
+// go through ONE inlined face solve (the HLLD solve is ~18 KB of SASS; one instance keeps the
+// kernel resident in the instruction cache):
+//   cell warp ty:  job 0 (3D)  z face k+1/2 of its column   (VL = V+(k) carried in smem)
+//                  job 1 (2D+) y face ty-1/2 of its cell
+//                  job 3       x face tx-1/2 of its cell
+//   edge warp:     job 1 (2D+) the y faces of row TY-1/2 (one per column)
+//                  job 2       the x faces of column TX-1/2 (one per row, lanes < TY)
+// so every warp runs at most 3 face solves per plane and the per-plane barriers do not wait
+// on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
 template <int DIM, int NV, int RS, int TY>
-__global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArgs a) {
+__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_stage(StageArgs a) {
   using S = StageSmem<DIM, NV, TY>;
-  constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH;
-  constexpr int NT = 32 * TY;
+  constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH, NT = S::NT;
+  constexpr int NC = 32 * TY;        // threads of the cell warps
   extern __shared__ double smem[];
   double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo)
-  double* Vpz = Vc + S::nVc;         // [NV][TY][TX] V+ (z) of plane k        (3D)
-  double* Fz = Vpz + S::nCol;        // [2][NV][TY][TX] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
+  double* Vpz = Vc + S::nVc;         // [NV][NC] V+ (z normal frame) of plane k   (3D)
+  double* Fz = Vpz + S::nCol;        // [2][NV][NC] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
   double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
   double* Fx = Fy + S::nFy;          // [NV][TY][TX+1] x-face fluxes of plane k
 
   const StageConsts& c = a.c;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const bool cellw = ty < TY;        // warp-uniform
   const int nx = a.nx, ny = a.ny, nzl = a.nz_loc;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int gx = x0 + tx, gy = y0 + ty;
-  const bool own = gx < nx && gy < ny;
+  const bool own = cellw && gx < nx && gy < ny;
   const size_t fstride = (size_t)nx * ny;
   const size_t pstride = fstride * NV;
   const int kb = blockIdx.z * a.kz;
@@ -166,16 +173,17 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
 #pragma unroll
     for (int f = 0; f < NV; ++f) Vc[(f * PH + r) * PW + col] = v[f];
   };
-  // plane k into Vc: interior (own cell) + x halo of the TY rows + y halo of the TX columns
+  // plane k into Vc: interior (cell warps, own cell) + x halo of the TY rows + y halo of the
+  // TX columns (all warps)
   auto load_plane = [&](int k, bool count_own) {
-    {
+    if (cellw) {
       double v[NV];
       convert_own(k, v, count_own);
       store_vc(ty + HY, tx + 2, v);
     }
     constexpr int NXH = 4 * TY;
     constexpr int NYH = (DIM >= 2) ? 4 * TX : 0;
-    for (int h = tid; h < NXH + NYH; h += NT) {
+    for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {  // the edge warp takes the first slots
       double v[NV];
       if (h < NXH) {
         const int r = h >> 2, w = h & 3;
@@ -195,16 +203,18 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
   int kstart = kb;
   if constexpr (DIM == 3) {
     // V+(kb-1) into Vpz; V(kb-1) as the centre of Vc (read by the z job of iteration kb-1)
-    double qA[NV], qB[NV], qC[NV], qp[NV], qm[NV];
-    convert_own(kb - 2, qA, false);
-    convert_own(kb - 1, qB, false);
-    convert_own(kb, qC, true);  // the counted conversion of plane kb
-    plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
-    double wp[NV];
-    to_normal<NV, 2>(qp, wp);  // Vpz is kept in the z normal frame
+    if (cellw) {
+      double qA[NV], qB[NV], qC[NV], qp[NV], qm[NV];
+      convert_own(kb - 2, qA, false);
+      convert_own(kb - 1, qB, false);
+      convert_own(kb, qC, true);  // the counted conversion of plane kb
+      plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
+      double wp[NV];
+      to_normal<NV, 2>(qp, wp);  // Vpz is kept in the z normal frame
 #pragma unroll
-    for (int f = 0; f < NV; ++f) Vpz[f * NT + tid] = wp[f];
-    store_vc(ty + HY, tx + 2, qB);
+      for (int f = 0; f < NV; ++f) Vpz[f * NC + tid] = wp[f];
+      store_vc(ty + HY, tx + 2, qB);
+    }
     kstart = kb - 1;
     __syncthreads();
   } else {
@@ -215,50 +225,49 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
   // ------------------------------------------------------------------ march over z
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
-    if constexpr (DIM == 3) {
-      // latency hiding: the own column of plane k+3 (first touched next iteration) into L2,
-      // and the own cell of plane k (re-read by the update at the end of this iteration) into L1
+    if (DIM == 3 && cellw) {
+      // latency hiding: own column of plane k+3 (first touched next iteration) into L2; own
+      // cell of planes k+1, k+2 (the z job) and of plane k (update; U^n in stage 2) into L1
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
         prefetch_l2(a.Uin + plane_off(k + 3 < nzl + a.gz ? k + 3 : k) + f * fstride + own_cell);
-        if (full) prefetch_l1(a.Uin + plane_off(k) + f * fstride + own_cell);
+        prefetch_l1(a.Uin + plane_off(k + 2) + f * fstride + own_cell);
+        if (full && a.stage == 2) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
       }
     }
-    const int jfirst = (DIM == 3) ? 0 : 1;
-    const int jlast = full ? 3 : 0;
 #pragma unroll 1
-    for (int job = jfirst; job <= jlast; ++job) {
-      // ---- select the face of this job
+    for (int job = 0; job <= 3; ++job) {
+      // ---- select the face of this job (warp-uniform activity)
       int d = 0, row = ty, col = tx;
-      bool active = true, cnt_right = false, cnt_face = false;
+      bool active, cnt_right = false, cnt_face = false;
       if (job == 0) {
+        active = DIM == 3 && cellw;
         d = 2;
         cnt_right = own && k + 1 < ke;
         cnt_face = own && (k + 1 < ke || a.zoff + k + 1 == a.nz_glob);
       } else if (job == 1) {
+        active = DIM >= 2 && full;
         d = 1;
-        active = DIM >= 2;
-        cnt_right = own;
-        cnt_face = own || (gy == ny && gx < nx);
-      } else if (job == 2) {
-        if (DIM >= 2 && ty == 0) {  // y faces of row TY - 1/2
-          d = 1;
+        if (cellw) {
+          cnt_right = own;
+          cnt_face = own || (gy == ny && gx < nx);
+        } else {  // edge warp: y faces of row TY - 1/2
           row = TY;
           cnt_face = (y0 + TY == ny) && gx < nx;
-        } else if (ty == ((DIM >= 2 && TY >= 2) ? 1 : 0) && tx < TY) {  // x faces of column TX - 1/2
-          d = 0;
-          row = tx;
-          col = TX;
-          cnt_face = (x0 + TX == nx) && (y0 + tx < ny);
-        } else {
-          active = false;
         }
+      } else if (job == 2) {  // edge warp: x faces of column TX - 1/2
+        active = !cellw && full && tx < TY;
+        d = 0;
+        row = tx;
+        col = TX;
+        cnt_face = (x0 + TX == nx) && (y0 + tx < ny);
       } else {
+        active = cellw && full;
         d = 0;
         cnt_right = own;
         cnt_face = own || (gx == nx && gy < ny);
       }
-      if (!active) continue;  // warp-uniform
+      if (!active) continue;
       // ---- gather the two face states (normal frame) with PLM
       // x/y jobs read Vc with the frame permutation folded into the field addresses
       // (component n of the normal frame of direction d is field fo[n]); PLM is
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
 #pragma unroll
           for (int f = 0; f < NV; ++f) {
             q0[f] = Vc[(f * PH + ty + HY) * PW + tx + 2];
-            wl[f] = Vpz[f * NT + tid];
+            wl[f] = Vpz[f * NC + tid];
           }
           convert_own(k + 1, q1, false);
           convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
@@ -286,7 +295,7 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
           to_normal<NV, 2>(qp, wp);
           to_normal<NV, 2>(qm, wr);
 #pragma unroll
-          for (int f = 0; f < NV; ++f) Vpz[f * NT + tid] = wp[f];
+          for (int f = 0; f < NV; ++f) Vpz[f * NC + tid] = wp[f];
         } else {
           const int s = (d == 0) ? 1 : PW;
           double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
         from_normal<NV, 2>(fn, fz);
         double* dst = Fz + ((k + 1) & 1) * S::nCol;
 #pragma unroll
-        for (int f = 0; f < NV; ++f) dst[f * NT + tid] = fz[f];
+        for (int f = 0; f < NV; ++f) dst[f * NC + tid] = fz[f];
       } else if (d == 1) {
 #pragma unroll
         for (int n = 0; n < NV; ++n) Fy[(fo[n] * (TY + 1) + row) * TX + col] = fn[n];
@@ -328,23 +337,31 @@ __global__ void __launch_bounds__(32 * TY, StageOcc<TY>::value) k_stage(StageArg
       __syncthreads();
       continue;
     }
-    __syncthreads();
-    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz)
+    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads are
+    // issued before the barrier so their latency overlaps the wait.
+    const size_t off = plane_off(k) + (size_t)gy * nx + gx;
+    double u0[NV], un[NV];
     if (own) {
-      const size_t off = plane_off(k) + (size_t)gy * nx + gx;
+#pragma unroll
+      for (int f = 0; f < NV; ++f) {
+        u0[f] = __ldg(a.Uin + off + f * fstride);
+        un[f] = (a.stage == 2) ? a.Un[off + f * fstride] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (own) {
       const double* fzn = Fz + ((k + 1) & 1) * S::nCol;
       const double* fzo = Fz + (k & 1) * S::nCol;
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
         double r = c.lam[0] * (Fx[(f * TY + ty) * (TX + 1) + tx + 1] - Fx[(f * TY + ty) * (TX + 1) + tx]);
         if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
-        if constexpr (DIM == 3) r = r + c.lam[2] * (fzn[f * NT + tid] - fzo[f * NT + tid]);
-        const double s = __ldg(a.Uin + off + f * fstride) - r;
+        if constexpr (DIM == 3) r = r + c.lam[2] * (fzn[f * NC + tid] - fzo[f * NC + tid]);
+        const double s = u0[f] - r;
         if (a.stage == 1) {
           a.Uout[off + f * fstride] = s;
         } else {
-          const double un = a.Un[off + f * fstride];
-          double v = 0.5 * (un + s);  // U^{n+1} = (U^n + U**)/2
+          double v = 0.5 * (un[f] + s);  // U^{n+1} = (U^n + U**)/2
           if (NV > 8 && f == NV - 1) v = v * c.damp;
           a.Uout[off + f * fstride] = v;
         }
@@ -495,15 +512,15 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.nz_loc + a.kz - 1) / a.kz);
-  kern<<<grid, 32 * TY, S::bytes, st>>>(a);
+  kern<<<grid, S::NT, S::bytes, st>>>(a);
   return cudaGetLastError();
 }
 
 #ifndef MHD_TY3
-#define MHD_TY3 6
+#define MHD_TY3 5
 #endif
 #ifndef MHD_TY2
-#define MHD_TY2 8
+#define MHD_TY2 5
 #endif
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
   if (dim == 3) {
