@@ -77,9 +77,15 @@ typedef struct {
 
 /* Multi-GPU: z-slab decomposition over nranks GPUs.  NULL => 1 GPU, the
  * current CUDA device.  nranks must divide n[2] with n[2]/nranks >= 2.  nccl_id comes from
- * mhd_nccl_get_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed). */
+ * mhd_nccl_get_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
+ * transport MHD_TRANSPORT_NCCL: one process per GPU, halos by ncclSend/ncclRecv overlapped
+ * with the interior of each stage, dt by ncclAllReduce(max).
+ * transport MHD_TRANSPORT_LOCAL: the nranks slabs live in ONE process on one device and are
+ * stepped together by mhd_group_step / mhd_group_compute_dt (halos by device copies); it
+ * exercises the identical decomposition, kernels and counters without NCCL (tests, 1 GPU). */
+enum { MHD_TRANSPORT_NCCL = 0, MHD_TRANSPORT_LOCAL = 1 };
 typedef struct {
-  int32_t rank, nranks, device, reserved;
+  int32_t rank, nranks, device, transport;
   uint8_t nccl_id[128];
 } mhd_dist;
 
@@ -136,6 +142,20 @@ int mhd_compute_dt(mhd_ctx* ctx, double* dt);
  * Collective with nranks > 1; asynchronous with respect to the host.  Also produces the
  * partial maxima the next mhd_compute_dt needs. */
 int mhd_step(mhd_ctx* ctx, double dt);
+
+/* In-process slab group (MHD_TRANSPORT_LOCAL): ctxs[r] is rank r of n, all on the current
+ * device and the same stream (ctxs[0]'s).  mhd_group_compute_dt returns the global dt (max
+ * over the slabs, exact) and caches c_h in every context; mhd_group_step runs, per RK stage,
+ * the halo copies of every slab and then the stage kernel of every slab.  The group runs on
+ * ctxs[0]'s stream: destroy the contexts in reverse rank order (rank 0 last). */
+int mhd_group_compute_dt(mhd_ctx* const* ctxs, int32_t n, double* dt);
+int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
+
+/* Halo plan of a z slab (pure host logic, no GPU): the 4 transfers of one RK stage in posting
+ * order, each as (peer rank or -1, 0 = send / 1 = recv, first storage plane, plane count);
+ * storage planes are 0..nz_loc+3 with the 2 ghost planes at each end.  Returns MHD_E_ARG on
+ * inconsistent arguments. */
+int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t plan[4][4]);
 
 /* Counters and the unphysical-state record (synchronising; collective when nranks > 1
  * only through mhd_compute_dt, which refreshes the global sums). */

@@ -46,6 +46,10 @@ struct mhd_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ncclComm_t comm = nullptr;
+  int transport = MHD_TRANSPORT_NCCL;
+  cudaStream_t comm_stream = nullptr;            // NCCL halo exchange (overlaps the interior)
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  mhd_ctx* const* group = nullptr;                // MHD_TRANSPORT_LOCAL: the slabs of this group
   int nsm = 148;
   int kz = 32;
   // cached step state
@@ -113,38 +117,88 @@ StageConsts make_consts(const mhd_ctx* c, double dt, double ch) {
   return k;
 }
 
-// a1 (z part): fill the 2 ghost planes on each side of array U (3D only)
-int fill_z_ghosts(mhd_ctx* c, double* U) {
+// a1 (z part).  Halo plan of one stage for a z slab: the transfers in posting order as
+// (peer, 0 send / 1 recv, first storage plane, planes).  Storage planes: 0,1 bottom ghosts,
+// 2..nz+1 interior, nz+2, nz+3 top ghosts.  Sends: top 2 interior planes -> up, bottom 2
+// interior planes -> down; receives: bottom ghosts <- down, top ghosts <- up.  The fixed
+// posting order (send up, recv down, send down, recv up) pairs correctly with nranks = 2,
+// where both neighbours are the same peer (NCCL matches per peer in posting order).
+int halo_plan(int rank, int nranks, long long nz_glob, int z_periodic, int plan[4][4]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || nz_glob % nranks != 0 || nz_glob / nranks < 2) return MHD_E_ARG;
+  const int nz = (int)(nz_glob / nranks);
+  const int up = (nranks > 1 && (z_periodic || rank < nranks - 1)) ? (rank + 1) % nranks : -1;
+  const int down = (nranks > 1 && (z_periodic || rank > 0)) ? (rank + nranks - 1) % nranks : -1;
+  const int rows[4][4] = {{up, 0, nz, 2}, {down, 1, 0, 2}, {down, 0, 2, 2}, {up, 1, nz + 2, 2}};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) plan[i][j] = rows[i][j];
+  return MHD_OK;
+}
+
+// local part of the z ghost fill of array `which` (0: U^n, 1: U*): periodic wrap on one slab,
+// zero-gradient copies at outflow domain ends
+int fill_z_ghosts_local(mhd_ctx* c, double* U) {
   if (c->dim < 3) return MHD_OK;
   const size_t pe = plane_elems(c), pb = pe * sizeof(double);
   const int nz = c->nzl, g = c->gz;
   auto P = [&](int zs) { return U + (size_t)zs * pe; };
   const bool peri = c->bc_lo[2] == MHD_BC_PERIODIC;
-  const bool bottom_is_edge = (c->rank == 0) && !peri;
-  const bool top_is_edge = (c->rank == c->nranks - 1) && !peri;
-  if (c->nranks == 1) {
-    if (peri) {
-      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
-      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
-    }
+  if (c->nranks == 1 && peri) {
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (bottom_is_edge) {  // outflow: U[-2] = U[-1] = U[0]
+  if (!peri && c->rank == 0) {  // outflow: U[-2] = U[-1] = U[0]
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(1), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (top_is_edge) {  // outflow: U[N] = U[N+1] = U[N-1]
+  if (!peri && c->rank == c->nranks - 1) {  // outflow: U[N] = U[N+1] = U[N-1]
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g + 1), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (c->nranks > 1) {
-    // fixed posting order on every rank (P = 2: both neighbours are the same peer; NCCL pairs
-    // sends and receives per peer in posting order)
-    NCCL_OR_RETURN(c, ncclGroupStart());
-    if (c->up >= 0) NCCL_OR_RETURN(c, ncclSend(P(nz), 2 * pe, ncclFloat64, c->up, c->comm, c->stream));
-    if (c->down >= 0) NCCL_OR_RETURN(c, ncclRecv(P(0), 2 * pe, ncclFloat64, c->down, c->comm, c->stream));
-    if (c->down >= 0) NCCL_OR_RETURN(c, ncclSend(P(g), 2 * pe, ncclFloat64, c->down, c->comm, c->stream));
-    if (c->up >= 0) NCCL_OR_RETURN(c, ncclRecv(P(nz + g), 2 * pe, ncclFloat64, c->up, c->comm, c->stream));
-    NCCL_OR_RETURN(c, ncclGroupEnd());
+  return MHD_OK;
+}
+
+// exchange part by NCCL on the comm stream (after `ev_ready` on the compute stream); records
+// `ev_halo` on the comm stream
+int exchange_nccl(mhd_ctx* c, double* U) {
+  const size_t pe = plane_elems(c);
+  int plan[4][4];
+  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, plan))
+    return set_err(c, MHD_E_ARG, "halo plan");
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_ready, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  NCCL_OR_RETURN(c, ncclGroupStart());
+  for (int i = 0; i < 4; ++i) {
+    if (plan[i][0] < 0) continue;
+    double* p = U + (size_t)plan[i][2] * pe;
+    const size_t cnt = (size_t)plan[i][3] * pe;
+    if (plan[i][1] == 0)
+      NCCL_OR_RETURN(c, ncclSend(p, cnt, ncclFloat64, plan[i][0], c->comm, c->comm_stream));
+    else
+      NCCL_OR_RETURN(c, ncclRecv(p, cnt, ncclFloat64, plan[i][0], c->comm, c->comm_stream));
+  }
+  NCCL_OR_RETURN(c, ncclGroupEnd());
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+  return MHD_OK;
+}
+
+// exchange part for an in-process group: receives are device copies from the peer slab's
+// array (the same array role: U^n or U*)
+int exchange_local(mhd_ctx* c, int which) {
+  const size_t pe = plane_elems(c), pb = pe * sizeof(double);
+  int plan[4][4];
+  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, plan))
+    return set_err(c, MHD_E_ARG, "halo plan");
+  double* mine = which == 0 ? c->U0 : c->U1;
+  for (int i = 0; i < 4; ++i) {
+    if (plan[i][0] < 0 || plan[i][1] != 1) continue;  // receives only
+    const mhd_ctx* peer = c->group[plan[i][0]];
+    const double* theirs = which == 0 ? peer->U0 : peer->U1;
+    // the peer sends its top interior planes to its up neighbour, bottom ones to its down
+    // neighbour: my bottom ghosts (recv from down) <- down's storage planes nz, nz+1;
+    // my top ghosts (recv from up) <- up's storage planes 2, 3
+    const int src = (plan[i][2] == 0) ? peer->nzl : 2;
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(mine + (size_t)plan[i][2] * pe, theirs + (size_t)src * pe, 2 * pb,
+                                      cudaMemcpyDeviceToDevice, c->stream));
   }
   return MHD_OK;
 }
@@ -177,7 +231,7 @@ void prof_drain(mhd_ctx* c) {
   c->ev_kind.clear();
 }
 
-int run_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   StageArgs a;
   a.Uin = stage == 1 ? c->U0 : c->U1;
   a.Un = c->U0;
@@ -193,6 +247,8 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.bcy[0] = c->bc_lo[1];
   a.bcy[1] = c->bc_hi[1];
   a.kz = c->kz;
+  a.zb = zb;
+  a.ze = ze;
   a.stage = stage;
   a.c = k;
   a.counters = c->dbuf + 2;
@@ -227,7 +283,7 @@ int reduce_and_read(mhd_ctx* c) {
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt launch: %s", cudaGetErrorString(e));
   unsigned long long* src = c->dbuf;
-  if (c->nranks > 1) {
+  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
     // maxima (exact on the int64 patterns of non-negative doubles), counter sums, bad-slot minima
     NCCL_OR_RETURN(c, ncclGroupStart());
     NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf, c->dred, 2, ncclUint64, ncclMax, c->comm, c->stream));
@@ -241,7 +297,8 @@ int reduce_and_read(mhd_ctx* c) {
   c->diag.p_floors = (int64_t)c->hbuf[2];
   c->diag.plm_fallbacks = (int64_t)c->hbuf[3];
   c->diag.hlld_to_hll = (int64_t)c->hbuf[4];
-  for (int s = 0; s < 3; ++s) {
+  // time order of the records: stage 1 and stage 2 of the last step, then the dt pass
+  for (int s : {1, 2, 0}) {
     if (c->hbuf[5 + s] != ~0ULL) {
       c->diag.bad_stage = s;
       c->diag.first_bad_cell = (int64_t)c->hbuf[5 + s];
@@ -335,6 +392,10 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->nv = 8 + c->scheme.glm;
   c->rank = dist ? dist->rank : 0;
   c->nranks = dist ? dist->nranks : 1;
+  if (dist && dist->transport != MHD_TRANSPORT_NCCL && dist->transport != MHD_TRANSPORT_LOCAL) {
+    delete c;
+    return MHD_E_ARG;
+  }
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks || (c->nranks > 1 && c->dim < 3) ||
       (c->n[2] % c->nranks) != 0 || (c->dim == 3 && c->n[2] / c->nranks < 2)) {
     delete c;
@@ -390,7 +451,14 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     mhd_destroy(c);
     return MHD_E_CUDA;
   }
-  if (c->nranks > 1) {
+  c->transport = dist ? dist->transport : MHD_TRANSPORT_NCCL;
+  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+      mhd_destroy(c);
+      return MHD_E_CUDA;
+    }
     ncclUniqueId id;
     memcpy(&id, dist->nccl_id, sizeof id);
     if (ncclCommInitRank(&c->comm, c->nranks, id, c->rank) != ncclSuccess) {
@@ -481,6 +549,8 @@ int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
 
 int mhd_compute_dt(mhd_ctx* c, double* dt) {
   if (!c || !dt) return MHD_E_ARG;
+  if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)
+    return set_err(c, MHD_E_STATE, "in-process slab group: use mhd_group_compute_dt");
   int rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
@@ -501,6 +571,8 @@ int mhd_compute_dt(mhd_ctx* c, double* dt) {
 
 int mhd_step(mhd_ctx* c, double dt) {
   if (!c) return MHD_E_ARG;
+  if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)
+    return set_err(c, MHD_E_STATE, "in-process slab group: use mhd_group_step");
   int rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
@@ -512,12 +584,98 @@ int mhd_step(mhd_ctx* c, double dt) {
   }
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
-  if ((rc = fill_z_ghosts(c, c->U0))) return rc;
-  if ((rc = run_stage(c, 1, k))) return rc;
-  if ((rc = fill_z_ghosts(c, c->U1))) return rc;
-  if ((rc = run_stage(c, 2, k))) return rc;
+  for (int stage = 1; stage <= 2; ++stage) {
+    double* U = stage == 1 ? c->U0 : c->U1;
+    if ((rc = fill_z_ghosts_local(c, U))) return rc;
+    if (c->nranks > 1 && c->dim == 3) {
+      // halo exchange on the comm stream, overlapped with the interior planes [2, nz-2)
+      // (their stencil never reads a ghost plane); then the 2 + 2 boundary planes
+      if ((rc = exchange_nccl(c, U))) return rc;
+      const int lo = 2 < c->nzl ? 2 : c->nzl, hi = c->nzl - 2 > lo ? c->nzl - 2 : lo;
+      if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
+      CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
+      if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
+    } else {
+      if ((rc = run_stage(c, stage, k, 0, c->nzl))) return rc;
+    }
+  }
   c->ch_valid = false;
   c->diag.steps += 1;
+  return MHD_OK;
+}
+
+int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t plan[4][4]) {
+  if (!plan) return MHD_E_ARG;
+  return halo_plan(rank, nranks, nz_glob, z_periodic, plan);
+}
+
+namespace {
+int check_group(mhd_ctx* const* ctxs, int32_t n) {
+  if (!ctxs || n < 1) return MHD_E_ARG;
+  for (int r = 0; r < n; ++r) {
+    mhd_ctx* c = ctxs[r];
+    if (!c || c->nranks != n || c->rank != r || (n > 1 && c->transport != MHD_TRANSPORT_LOCAL)) return MHD_E_ARG;
+    if (c->sticky != MHD_OK) return set_err(c, MHD_E_STATE, "context in error state %d", c->sticky);
+    if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+    c->group = ctxs;
+    if (r > 0 && c->stream != ctxs[0]->stream) {  // one stream for the whole group
+      if (c->own_stream && c->stream) {
+        cudaStreamSynchronize(c->stream);
+        cudaStreamDestroy(c->stream);
+      }
+      c->stream = ctxs[0]->stream;
+      c->own_stream = false;
+    }
+  }
+  return MHD_OK;
+}
+}  // namespace
+
+int mhd_group_compute_dt(mhd_ctx* const* ctxs, int32_t n, double* dt) {
+  int rc = check_group(ctxs, n);
+  if (rc || !dt) return rc ? rc : MHD_E_ARG;
+  double M = 0.0, S = 0.0;
+  for (int r = 0; r < n; ++r) {  // exact maxima: the order over slabs does not matter
+    mhd_ctx* c = ctxs[r];
+    if ((rc = reduce_and_read(c))) return rc;
+    double m, sx;
+    memcpy(&m, &c->hbuf[0], sizeof m);
+    memcpy(&sx, &c->hbuf[1], sizeof sx);
+    M = m > M ? m : M;
+    S = sx > S ? sx : S;
+  }
+  if (!std::isfinite(M) || !(M > 0.0)) return set_err(ctxs[0], MHD_E_UNPHYSICAL, "signal speed maximum");
+  *dt = ctxs[0]->cfl / M;
+  for (int r = 0; r < n; ++r) {
+    ctxs[r]->ch = S;
+    ctxs[r]->ch_valid = true;
+  }
+  return MHD_OK;
+}
+
+int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
+  int rc = check_group(ctxs, n);
+  if (rc) return rc;
+  if (!(dt > 0.0) || !std::isfinite(dt)) return MHD_E_ARG;
+  for (int r = 0; r < n; ++r)
+    if (!ctxs[r]->ch_valid) return set_err(ctxs[r], MHD_E_STATE, "call mhd_group_compute_dt first");
+  for (int stage = 1; stage <= 2; ++stage) {
+    for (int r = 0; r < n; ++r) {
+      mhd_ctx* c = ctxs[r];
+      if ((rc = fill_z_ghosts_local(c, stage == 1 ? c->U0 : c->U1))) return rc;
+      if (n > 1 && (rc = exchange_local(c, stage == 1 ? 0 : 1))) return rc;
+    }
+    for (int r = 0; r < n; ++r) {
+      mhd_ctx* c = ctxs[r];
+      const StageConsts k = make_consts(c, dt, c->ch);
+      if ((rc = run_stage(c, stage, k, 0, c->nzl))) return rc;
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    ctxs[r]->ch_valid = false;
+    ctxs[r]->diag.steps += 1;
+  }
   return MHD_OK;
 }
 
@@ -533,6 +691,9 @@ void mhd_destroy(mhd_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   if (c->U0) cudaFree(c->U0);
   if (c->U1) cudaFree(c->U1);
   if (c->dbuf) cudaFree(c->dbuf);

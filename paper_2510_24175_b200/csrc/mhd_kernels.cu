@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
   const bool own = cellw && gx < nx && gy < ny;
   const size_t fstride = (size_t)nx * ny;
   const size_t pstride = fstride * NV;
-  const int kb = blockIdx.z * a.kz;
-  const int ke = min(kb + a.kz, nzl);
+  const int kb = a.zb + blockIdx.z * a.kz;  // this CTA's z chunk inside [zb, ze)
+  const int ke = min(kb + a.kz, a.ze);
   int cnt_floor = 0, cnt_fb = 0, cnt_hll = 0;
   unsigned long long badidx = ULLONG_MAX;
 
@@ -511,7 +511,8 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.nz_loc + a.kz - 1) / a.kz);
+  if (a.ze <= a.zb) return cudaSuccess;
+  dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.ze - a.zb + a.kz - 1) / a.kz);
   kern<<<grid, S::NT, S::bytes, st>>>(a);
   return cudaGetLastError();
 }

@@ -20,6 +20,7 @@ struct StageArgs {
   long long nz_glob;  // global nz
   int bcx[2], bcy[2]; // 0 periodic, 1 outflow
   int kz;             // z planes per CTA
+  int zb, ze;         // local z range of cells this launch updates (interior/boundary split)
   int stage;          // 1 or 2
   StageConsts c;
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]

@@ -27,7 +27,9 @@ _NAMES = {0: "MHD_OK", 1: "MHD_E_ARG", 2: "MHD_E_STATE", 3: "MHD_E_CUDA", 4: "MH
 # every symbol include/mhd.h declares (checked by the CPU test suite)
 EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_box", "mhd_device_bytes",
            "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
-           "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version")
+           "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
+           "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan")
+TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
 class Grid(C.Structure):
@@ -44,7 +46,7 @@ class Scheme(C.Structure):
 
 
 class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("device", C.c_int32), ("transport", C.c_int32),
                 ("nccl_id", C.c_uint8 * 128)]
 
 
@@ -94,6 +96,9 @@ def load() -> C.CDLL:
     L.mhd_version.restype = C.c_char_p
     L.mhd_profile_enable.argtypes = [P, C.c_int32]
     L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.mhd_group_compute_dt.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(C.c_double)]
+    L.mhd_group_step.argtypes = [C.POINTER(P), C.c_int32, C.c_double]
+    L.mhd_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]
     _lib = L
     return L
 
@@ -108,6 +113,16 @@ def nccl_unique_id() -> bytes:
     if rc:
         raise MhdError(rc, "ncclGetUniqueId failed")
     return bytes(buf)
+
+
+def halo_plan(rank: int, nranks: int, nz_glob: int, z_periodic: bool = True):
+    """The 4 transfers of one RK stage for a z slab: rows (peer, 0 send / 1 recv, first storage
+    plane, planes) in posting order (pure host logic of libmhd, usable without a GPU)."""
+    buf = (C.c_int32 * 16)()
+    rc = load().mhd_halo_plan(rank, nranks, nz_glob, 1 if z_periodic else 0, buf)
+    if rc:
+        raise MhdError(rc, "mhd_halo_plan")
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(4)]
 
 
 def _ptr_of(U):
@@ -128,7 +143,7 @@ class Solver:
     """One libmhd context: the state of this rank's slab on one GPU."""
 
     def __init__(self, problem: "_inputs.Problem", rank: int = 0, nranks: int = 1, device: int = -1,
-                 nccl_id: Optional[bytes] = None, stream=None):
+                 nccl_id: Optional[bytes] = None, stream=None, transport: int = TRANSPORT_NCCL):
         L = load()
         self.problem = problem
         g = Grid()
@@ -143,7 +158,7 @@ class Solver:
                     float(problem.p_floor))
         dist = None
         if nranks > 1 or device >= 0:
-            dist = Dist(rank, nranks, device, 0)
+            dist = Dist(rank, nranks, device, transport)
             if nccl_id is not None:
                 C.memmove(dist.nccl_id, nccl_id, 128)
         h = C.c_void_p()
@@ -247,3 +262,59 @@ class Solver:
             log.append(dt)
             t = t + dt
         return np.array(log, dtype=np.float64)
+
+
+class SolverGroup:
+    """nranks z slabs of one problem in this process on one device (MHD_TRANSPORT_LOCAL): the
+    decomposition of the multi-GPU path (slab plan, halo planes, counters, dt reduction) with
+    device copies in place of NCCL.  Used to check decomposition invariance on one GPU."""
+
+    def __init__(self, problem: "_inputs.Problem", nranks: int):
+        self.problem = problem
+        self.slabs = [Solver(problem, rank=r, nranks=nranks, transport=TRANSPORT_LOCAL) for r in range(nranks)]
+        self._arr = (C.c_void_p * nranks)(*[s._h.value for s in self.slabs])
+        self._L = load()
+
+    def _check(self, rc):
+        if rc:
+            msgs = "; ".join(self._L.mhd_last_error(s._h).decode() for s in self.slabs)
+            raise MhdError(rc, msgs)
+
+    def set_state(self, U):
+        """U: the global interior state [nvar][nz][ny][nx] (numpy)."""
+        for s in self.slabs:
+            z0, nz = s.offset[2], s.extent[2]
+            s.set_state(np.ascontiguousarray(U[:, z0:z0 + nz]))
+
+    def get_state(self):
+        return np.concatenate([s.get_state() for s in self.slabs], axis=1)
+
+    def compute_dt(self) -> float:
+        dt = C.c_double()
+        self._check(self._L.mhd_group_compute_dt(self._arr, len(self.slabs), C.byref(dt)))
+        return dt.value
+
+    def step(self, dt: float) -> None:
+        self._check(self._L.mhd_group_step(self._arr, len(self.slabs), float(dt)))
+
+    def run(self, nsteps: int, t_end: float = 0.0):
+        log, t = [], 0.0
+        while len(log) < nsteps and (t_end <= 0.0 or t < t_end):
+            dt = self.compute_dt()
+            if t_end > 0.0 and t + dt > t_end:
+                dt = t_end - t
+            self.step(dt)
+            log.append(dt)
+            t = t + dt
+        return np.array(log, dtype=np.float64)
+
+    def diag(self) -> dict:
+        ds = [s.diag() for s in self.slabs]
+        out = {k: sum(d[k] for d in ds) for k in ("p_floors", "plm_fallbacks", "hlld_to_hll")}
+        out["steps"] = ds[0]["steps"]
+        return out
+
+    def destroy(self):
+        # rank 0 owns the group's stream: free it last
+        for s in reversed(self.slabs):
+            s.destroy()

@@ -1,0 +1,96 @@
+"""N > 1 host logic on CPU with torch.distributed (gloo, world_size 2): the slab halo plan
+exported by libmhd (mhd_halo_plan, the same function mhd_step uses to post its NCCL
+send/recv) is executed with gloo point-to-point on numpy slabs in libmhd's storage layout
+[z + 2][f][y][x]; every ghost plane must equal the neighbour's interior plane bitwise, i.e.
+the decomposition reproduces the periodic (or outflow-edge) ghost fill of the global array
+(SPEC.md:102-110 halo_exchange examples).  Also: the 128-byte NCCL unique
+id of rank 0 reaches every rank through the torch.distributed broadcast (bench.py's path)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, nz_glob, periodic, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_24175_b200 import mhd
+        nv, ny, nx = 9, 4, 5
+        rng = np.random.default_rng(1234)
+        G = rng.standard_normal((nz_glob, nv, ny, nx))  # global interior, storage order [z][f][y][x]
+        nz = nz_glob // world
+        z0 = rank * nz
+        S = np.full((nz + 4, nv, ny, nx), np.nan)
+        S[2:nz + 2] = G[z0:z0 + nz]
+        plan = mhd.halo_plan(rank, world, nz_glob, periodic)
+        reqs = []
+        for peer, kind, first, count in plan:  # posting order of the plan
+            if peer < 0:
+                continue
+            buf = torch.from_numpy(S[first:first + count])
+            if kind == 0:
+                reqs.append(dist.isend(buf.contiguous(), dst=peer))
+            else:
+                reqs.append((dist.irecv(buf, src=peer), buf))
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+            else:
+                r.wait()
+        ok = True
+        for g, zglob in ((0, z0 - 2), (1, z0 - 1), (nz + 2, z0 + nz), (nz + 3, z0 + nz + 1)):
+            if 0 <= zglob < nz_glob or periodic:
+                if not np.array_equal(S[g], G[zglob % nz_glob]):
+                    ok = False
+            else:
+                ok = ok and np.isnan(S[g]).all()  # domain edge: filled locally (outflow copy)
+        ids = [mhd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        q.put((rank, ok, ids[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_two_rank_halo_plan_with_gloo(periodic):
+    from paper_2510_24175_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 12, periodic, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    assert res[0][2] == res[1][2] and len(res[0][2]) == 128
+
+
+def test_halo_plan_shapes():
+    from paper_2510_24175_b200 import build, mhd
+    build.build()
+    # P = 1: no peers; P = 4 periodic: ring neighbours; P = 4 outflow: no wrap at the ends
+    assert all(r[0] == -1 for r in mhd.halo_plan(0, 1, 64))
+    assert [r[0] for r in mhd.halo_plan(0, 4, 64)] == [1, 3, 3, 1]
+    assert [r[0] for r in mhd.halo_plan(0, 4, 64, False)] == [1, -1, -1, 1]
+    assert [r[0] for r in mhd.halo_plan(3, 4, 64, False)] == [-1, 2, 2, -1]
+    assert mhd.halo_plan(1, 4, 64)[0] == (2, 0, 16, 2) and mhd.halo_plan(1, 4, 64)[3] == (2, 1, 18, 2)
+    with pytest.raises(mhd.MhdError):
+        mhd.halo_plan(0, 3, 64)  # 3 does not divide 64

@@ -236,3 +236,67 @@ def test_ot3d_256_full_size_parity(mhd):
     U0 = I.orszag_tang_3d_ic(p)
     res = run_both(mhd, p, U0, 2)
     assert_parity(*res)
+
+
+# ---------------------------------------------------------------------------------------------
+# decomposition invariance: P z-slabs == 1 domain, bitwise
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_group_bitwise_equals_single_domain(mhd, P):
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(6)
+    U1 = s.get_state()
+    d1 = s.diag()
+    s.destroy()
+    g = mhd.SolverGroup(p, P)
+    g.set_state(U0)
+    logP = g.run(6)
+    UP = g.get_state()
+    dP = g.diag()
+    g.destroy()
+    assert np.array_equal(log1, logP)
+    assert np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k]
+
+
+def test_slab_group_outflow_z_matches_oracle(mhd):
+    """the outflow shock tube along z split over 4 slabs (edge ranks copy, inner ranks exchange)"""
+    n = 48
+    p = I.Problem("bwz", (8, 8, n), bc=(I.OUTFLOW,) * 3, gamma=2.0, glm=1, riemann=I.HLLD)
+    U1 = I.brio_wu_ic(I.brio_wu(n).replace(glm=1))[:, 0, 0, :]
+    U = np.zeros(p.shape)
+    for f in range(9):
+        src = f
+        if 1 <= f <= 3:
+            src = 1 + (f - 1 - 2) % 3
+        if 5 <= f <= 7:
+            src = 5 + (f - 5 - 2) % 3
+        U[f] = U1[src][:, None, None]
+    o = oracle.Oracle(p, U)
+    log_o = o.run(30)
+    g = mhd.SolverGroup(p, 4)
+    g.set_state(U)
+    log_g = g.run(30)
+    Ug = g.get_state()
+    g.destroy()
+    assert np.array_equal(log_o, log_g)
+    assert np.all(rel_linf(Ug, o.U) <= TOL)
+
+
+def test_blast_weak_layout_two_cubes(mhd):
+    """configs[3] layout (one blast per unit cube along z) on 2 slabs vs the oracle"""
+    p = I.blast_3d(16, cubes=2)
+    U0 = I.blast_3d_ic(p)
+    o = oracle.Oracle(p, U0)
+    log_o = o.run(8)
+    g = mhd.SolverGroup(p, 2)
+    g.set_state(U0)
+    log_g = g.run(8)
+    Ug = g.get_state()
+    g.destroy()
+    assert np.array_equal(log_o, log_g)
+    assert np.all(rel_linf(Ug, o.U) <= TOL)
