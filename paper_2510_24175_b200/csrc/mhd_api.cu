@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -417,17 +418,29 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   const bool zper = c->bc_lo[2] == MHD_BC_PERIODIC;
   c->up = (c->nranks > 1 && (zper || c->rank < c->nranks - 1)) ? (c->rank + 1) % c->nranks : -1;
   c->down = (c->nranks > 1 && (zper || c->rank > 0)) ? (c->rank + c->nranks - 1) % c->nranks : -1;
-  // z chunk per CTA: enough CTAs for ~4 waves of 2 CTAs/SM, at least 8 planes per chunk
+  // z chunk per CTA (3D): the CTAs of one stage launch run in waves of nsm x (resident CTAs
+  // per SM); a chunk of kz planes costs ~kz + 1.5 plane-times (the prologue solves one extra z
+  // face and converts 2 extra planes).  Pick the chunk count minimising waves x chunk cost
+  // (MHD_KZ overrides, for measurements).
   {
-    const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + mhd::stage_tile_rows(c->dim) - 1) /
-                                                               mhd::stage_tile_rows(c->dim));
-    const long long want = (long long)c->nsm * 2 * 4;
-    long long chunks = (want + tiles - 1) / tiles;
-    if (chunks < 1) chunks = 1;
-    long long kz = (c->nzl + chunks - 1) / chunks;
-    if (kz < 8) kz = 8;
-    if (kz > c->nzl) kz = c->nzl;
-    c->kz = (int)kz;
+    const int ty = mhd::stage_tile_rows(c->dim);
+    const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + ty - 1) / ty);
+    const long long slots = (long long)c->nsm * mhd::stage_ctas_per_sm(c->dim, c->nv, c->scheme.riemann);
+    long long best_kz = c->nzl;
+    double best = 1e300;
+    for (long long chunks = 1; chunks <= c->nzl; ++chunks) {
+      const long long kz = (c->nzl + chunks - 1) / chunks;
+      const long long nch = (c->nzl + kz - 1) / kz;
+      const long long waves = (tiles * nch + slots - 1) / slots;
+      const double cost = (double)waves * ((double)kz + 1.5);
+      if (cost < best - 1e-9) {
+        best = cost;
+        best_kz = kz;
+      }
+    }
+    const char* env = getenv("MHD_KZ");
+    if (env && atoi(env) > 0) best_kz = atoi(env) < c->nzl ? atoi(env) : c->nzl;
+    c->kz = (int)(best_kz > 0 ? best_kz : 1);
   }
   c->arr_elems = plane_elems(c) * (size_t)(c->nzl + 2 * c->gz);
   cudaError_t e1 = cudaMalloc(&c->U0, c->arr_elems * sizeof(double));

@@ -542,6 +542,22 @@ cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaS
 
 int stage_tile_rows(int dim) { return dim == 3 ? MHD_TY3 : (dim == 2 ? MHD_TY2 : 1); }
 
+template <int DIM, int NV, int RS, int TY>
+static int ctas_per_sm_t() {
+  using S = StageSmem<DIM, NV, TY>;
+  auto kern = k_stage<DIM, NV, RS, TY>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, S::NT, S::bytes) != cudaSuccess) n = 1;
+  return n > 0 ? n : 1;
+}
+
+int stage_ctas_per_sm(int dim, int nv, int riemann) {
+  if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3>() : ctas_per_sm_t<3, 9, 0, MHD_TY3>();
+  if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2>() : ctas_per_sm_t<2, 9, 0, MHD_TY2>();
+  return 1;
+}
+
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st) {
   const size_t ncell = (size_t)a.nx * a.ny * a.nz_loc;
   size_t blocks = (ncell + 255) / 256;
