@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "mhd_device.cuh"
@@ -506,14 +507,17 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
   using S = StageSmem<DIM, NV, TY>;
   auto kern = k_stage<DIM, NV, RS, TY>;
   static bool attr_set = false;
+  static size_t extra = 0;  // MHD_EXTRA_SMEM (bytes): measurement knob for the L1 carve-out
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    const char* e_ = getenv("MHD_EXTRA_SMEM");
+    extra = e_ ? (size_t)atol(e_) : 0;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(S::bytes + extra));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   if (a.ze <= a.zb) return cudaSuccess;
   dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.ze - a.zb + a.kz - 1) / a.kz);
-  kern<<<grid, S::NT, S::bytes, st>>>(a);
+  kern<<<grid, S::NT, S::bytes + extra, st>>>(a);
   return cudaGetLastError();
 }
 
