@@ -101,9 +101,35 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
-def build_problem(n_gpus: int, n: int):
+WORKLOADS = {
+    "ot3d": "3D Orszag-Tang (BASELINE configs[2] at 256^3, configs[4] at 1024^3)",
+    "blast3d": "3D MHD blast, one blast per GPU cube (BASELINE configs[3], 512^3 per GPU)",
+    "cpa3d": "3D circularly polarised Alfven wave along the diagonal (SURVEY §8(f) row 1)",
+}
+
+
+def build_problem(workload: str, n_gpus: int, n: int):
+    """per-GPU n^3 cube; with N GPUs the box is n x n x (n N) with z extent N (weak scaling)"""
     from paper_2510_24175_b200 import inputs as I
-    return I.orszag_tang_3d(n, nz=n * n_gpus, z_extent=float(n_gpus))
+    if workload == "ot3d":
+        return I.orszag_tang_3d(n, nz=n * n_gpus, z_extent=float(n_gpus))
+    if workload == "blast3d":
+        return I.blast_3d(n, cubes=n_gpus)
+    if workload == "cpa3d":
+        return I.cpa_3d(n).replace(n=(n, n, n * n_gpus), hi=(1.0, 1.0, float(n_gpus)))
+    raise ValueError(workload)
+
+
+def build_ic(workload: str, p, z0: int, z1: int, chunk: int = 64):
+    """initial condition of global planes [z0, z1), generated in z chunks into one array (keeps
+    the host peak near the array size for 1024^3)"""
+    from paper_2510_24175_b200 import inputs as I
+    fn = {"ot3d": I.orszag_tang_3d_ic, "blast3d": I.blast_3d_ic, "cpa3d": I.cpa_3d_ic}[workload]
+    U = np.empty((p.nvar, z1 - z0, p.n[1], p.n[0]), dtype=np.float64)
+    for a in range(z0, z1, chunk):
+        b = min(z1, a + chunk)
+        U[:, a - z0:b - z0] = fn(p, z_range=(a, b))
+    return U
 
 
 def cpu_info():
@@ -115,14 +141,14 @@ def cpu_info():
         return "unknown"
 
 
-def oracle_sample(n: int, nz_s: int, steps: int, warmup: int):
+def oracle_sample(workload: str, n: int, nz_s: int, steps: int, warmup: int):
     """The CPU oracle, as it stands, on a bounded sample of the workload: the first nz_s planes of
-    the n^3 OT-3D initial condition as a periodic n x n x nz_s slab (same per-cell work)."""
+    the n^3 initial condition as a periodic n x n x nz_s slab (same per-cell work)."""
     import oracle
-    from paper_2510_24175_b200 import inputs as I
-    full = I.orszag_tang_3d(n)
-    p = full.replace(n=(n, n, nz_s), hi=(1.0, 1.0, nz_s / n))
-    U = I.orszag_tang_3d_ic(full, z_range=(0, nz_s))
+    full = build_problem(workload, 1, n)
+    dz = (full.hi[2] - full.lo[2]) / full.n[2]
+    p = full.replace(n=(n, n, nz_s), hi=(full.hi[0], full.hi[1], full.lo[2] + nz_s * dz))
+    U = build_ic(workload, full, 0, nz_s)
     o = oracle.Oracle(p, U)
     for _ in range(warmup):
         dt, ch = o.compute_dt()
@@ -138,15 +164,16 @@ def oracle_sample(n: int, nz_s: int, steps: int, warmup: int):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    n, nz_s = args.n, max(4, args.n // 4)
-    v, el, cores, p = oracle_sample(n, nz_s, args.steps, args.warmup)
+    n = args.n
+    nz_s = max(4, min(n, (256 ** 3 // 4) // (n * n)))  # ~4.2 M cells per step
+    v, el, cores, p = oracle_sample(args.workload, n, nz_s, args.steps, args.warmup)
     sample = (f"CPU oracle (oracle/mhd_oracle.c, gcc -O2 -ffp-contract=off, OpenMP {cores} threads), "
               f"{args.steps} timed steps after {args.warmup} warm-up of a {n}x{n}x{nz_s} periodic slab of the "
-              f"{n}^3 OT-3D IC (1/{n // nz_s} of the workload per step)")
+              f"{n}^3 {args.workload} IC ({nz_s}/{n} of the workload's planes per step)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"ot3d_{n}", "cells_per_step": p.cells, "sample": f"{n}x{n}x{nz_s}",
+            "config": {"workload": f"{args.workload}_{n}^3_per_gpu", "cells_per_step": p.cells, "sample": f"{n}x{n}x{nz_s}",
                        "parallelism": "host cores"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu": cpu_info()},
@@ -161,6 +188,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mhd", choices=["mhd", "reference"])
     ap.add_argument("--n", type=int, default=256, help="cells per axis per GPU (configs[2]: 256)")
+    ap.add_argument("--workload", default="ot3d", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=256, help="cpu_baseline sample: planes of the grid")
@@ -183,7 +211,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    p = build_problem(world, args.n)
+    p = build_problem(args.workload, world, args.n)
     nz_loc = p.n[2] // world
     nccl_id = None
     if world > 1:
@@ -193,9 +221,11 @@ def main():
     s = mhd.Solver(p, rank=rank, nranks=world, device=local_rank, nccl_id=nccl_id)
     stream = torch.cuda.current_stream()
     s.set_stream(stream)
-    U0 = I.orszag_tang_3d_ic(p, z_range=(rank * nz_loc, (rank + 1) * nz_loc))
-    U0d = torch.from_numpy(U0).cuda()
-    s.set_state(U0d)
+    U0 = build_ic(args.workload, p, rank * nz_loc, (rank + 1) * nz_loc)
+    if U0.nbytes <= 8 << 30:
+        s.set_state(torch.from_numpy(U0).cuda())
+    else:  # 1024^3: host copy-in (the library stages through its second array: no third array)
+        s.set_state(U0)
 
     def barrier():
         if world > 1:
@@ -263,7 +293,7 @@ def main():
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and U0.nbytes <= 8 << 30:
         Uh = torch.from_numpy(U0).pin_memory()
         Uo = torch.empty_like(Uh).pin_memory()
         ke = max(1, min(args.steps, 5))
@@ -286,18 +316,18 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        nz_s = min(args.cpu_planes, args.n)
-        v, el, cores, pp = oracle_sample(args.n, nz_s, 1, 0)
+        nz_s = min(args.cpu_planes, args.n, max(4, (256 ** 3) // (args.n * args.n)))
+        v, el, cores, pp = oracle_sample(args.workload, args.n, nz_s, 1, 0)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_info(),
                "sample": f"1 step (compute_dt + RK2 step) of a {args.n}x{args.n}x{nz_s} periodic slab of the "
-                         f"{args.n}^3 OT-3D IC, {el:.1f} s on {cores} OpenMP threads"}
+                         f"{args.n}^3 {args.workload} IC, {el:.1f} s on {cores} OpenMP threads"}
 
     s.destroy()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"ot3d_{args.n}^3_per_gpu (BASELINE configs[2]; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
+                "config": {"workload": f"{args.workload}_{args.n}^3_per_gpu ({WORKLOADS[args.workload]}; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
                            "scheme": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4", "cells": cells,
                            "parallelism": f"z-slab x{world}", "l2": "inputs larger than L2 (2 x 1.27 GB arrays per GPU)"},
                 "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * 3,

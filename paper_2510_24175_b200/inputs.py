@@ -218,6 +218,42 @@ def cpa_2d_ic(p: Problem, amp: float = 0.1) -> np.ndarray:
     return prim_to_cons_ic(p, 1.0, V[0], V[1], V[2], 0.1, B[0], B[1], B[2])
 
 
+def cpa_3d(n=64, limiter=MC, riemann=HLLD) -> Problem:
+    """3D circularly polarised Alfven wave (the paper's second gPLUTO benchmark, PAPER.md:176-181
+    §4.2; parameters deferred there, reading R23 / SPEC.md:140): rho = 1, p = 0.1, B_par = 1,
+    amplitude 0.1, propagating along the box diagonal n = (1,1,1)/sqrt3 of the periodic unit cube
+    (wave vector 2pi(1,1,1): one wavelength 1/sqrt3 per axis period); v_A = 1, so the exact
+    solution returns to the initial condition after one period t = 1/sqrt3."""
+    return Problem("cpa3d", (n, n, n), gamma=5.0 / 3.0, limiter=limiter, riemann=riemann, glm=1,
+                   t_end=1.0 / math.sqrt(3.0))
+
+
+def cpa_3d_fields(p: Problem, t: float = 0.0, amp: float = 0.1, z_range=None):
+    """primitive fields (rho, v, p, B) of the exact 3D CPA solution at time t (cell centres)."""
+    sub = p
+    if z_range is not None:
+        k0, k1 = z_range
+        dz = (p.hi[2] - p.lo[2]) / p.n[2]
+        sub = p.replace(n=(p.n[0], p.n[1], k1 - k0), lo=(p.lo[0], p.lo[1], p.lo[2] + k0 * dz),
+                        hi=(p.hi[0], p.hi[1], p.lo[2] + k1 * dz))
+    X, Y, Z = mesh(sub)
+    s3 = math.sqrt(3.0)
+    n = np.array([1.0, 1.0, 1.0]) / s3
+    t1 = np.array([1.0, -1.0, 0.0]) / math.sqrt(2.0)
+    t2 = np.array([1.0, 1.0, -2.0]) / math.sqrt(6.0)
+    ph = 2.0 * math.pi * ((X + Y + Z) - s3 * t)  # phase moves at v_A = 1 along n
+    b1, b2 = amp * np.sin(ph), amp * np.cos(ph)
+    B = [n[c] + b1 * t1[c] + b2 * t2[c] for c in range(3)]
+    V = [-(b1 * t1[c] + b2 * t2[c]) for c in range(3)]  # v_perp = -B_perp/sqrt(rho): moves along +n
+    return 1.0, V, 0.1, B
+
+
+def cpa_3d_ic(p: Problem, z_range=None) -> np.ndarray:
+    rho, V, pr, B = cpa_3d_fields(p, 0.0, z_range=z_range)
+    sub = p if z_range is None else p.replace(n=(p.n[0], p.n[1], z_range[1] - z_range[0]))
+    return prim_to_cons_ic(sub, rho, V[0], V[1], V[2], pr, B[0], B[1], B[2])
+
+
 def with_noise(U: np.ndarray, p: Problem, amp: float = 1e-3, seed: int = 2510) -> np.ndarray:
     """'OT + noise' stress IC: multiplies rho and E by (1 + amp*U(-1,1)), seeded."""
     rng = np.random.default_rng(seed)
@@ -262,4 +298,5 @@ CONFIGS = {
     "ot3d_256": (lambda: orszag_tang_3d(256), orszag_tang_3d_ic),
     "blast3d_512": (lambda: blast_3d(512), blast_3d_ic),
     "ot3d_1024": (lambda: orszag_tang_3d(1024), orszag_tang_3d_ic),
+    "cpa3d_256": (lambda: cpa_3d(256), cpa_3d_ic),
 }

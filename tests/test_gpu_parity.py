@@ -300,3 +300,10 @@ def test_blast_weak_layout_two_cubes(mhd):
     g.destroy()
     assert np.array_equal(log_o, log_g)
     assert np.all(rel_linf(Ug, o.U) <= TOL)
+
+
+def test_cpa3d_full_period(mhd):
+    """§8(f) row 1: 3D CPA (the paper's second workload) for one full period at 24^3, bitwise."""
+    p = I.cpa_3d(24)
+    res = run_both(mhd, p, I.cpa_3d_ic(p), 10 ** 6, p.t_end)
+    assert_parity(*res)

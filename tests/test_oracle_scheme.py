@@ -231,3 +231,37 @@ def test_unphysical_state_reported():
     assert e.value.rc == 6
     c = e.value.counters.as_dict()
     assert c["bad_stage"] == 0 and c["first_bad_cell"] == (3 * 8 + 2) * 8 + 5
+
+
+@pytest.mark.slow
+def test_cpa_3d_oblique_convergence():
+    """§8(f) row 1: the paper's second benchmark, the 3D circularly polarised Alfven wave
+    (PAPER.md:176-181), propagating along the box diagonal; an exact nonlinear solution that
+    returns to the IC after one period (R23).  L1(By) error falls at second order."""
+    errs = []
+    for n in (8, 16, 32):
+        p = I.cpa_3d(n)
+        U0 = I.cpa_3d_ic(p)
+        o = oracle.Oracle(p, U0)
+        o.run(10 ** 6, p.t_end)
+        assert abs(o.t - p.t_end) < 1e-12
+        errs.append(np.abs(o.U[6] - U0[6]).mean() / 0.1)
+        assert o.counters()["plm_fallbacks"] == 0 and o.counters()["p_floors"] == 0
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert orders[-1] >= 1.8, (errs, orders)
+    assert errs[-1] <= 0.02
+
+
+def test_cpa_3d_exact_solution_definition():
+    """the IC generator's exact solution is consistent: at t = one period it equals t = 0, it is
+    divergence-free and |B_perp| is constant (circular polarisation)."""
+    p = I.cpa_3d(12)
+    r0, V0, p0, B0 = I.cpa_3d_fields(p, 0.0)
+    r1, V1, p1, B1 = I.cpa_3d_fields(p, p.t_end)
+    for c in range(3):
+        assert np.allclose(B0[c], B1[c], atol=1e-12) and np.allclose(V0[c], V1[c], atol=1e-12)
+    n = np.ones(3) / math.sqrt(3.0)
+    Bpar = sum(B0[c] * n[c] for c in range(3))
+    assert np.allclose(Bpar, 1.0, atol=1e-14)
+    bperp2 = sum(B0[c] ** 2 for c in range(3)) - Bpar ** 2
+    assert np.allclose(bperp2, 0.01, atol=1e-14)
