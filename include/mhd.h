@@ -50,6 +50,7 @@ enum {
 enum { MHD_BC_PERIODIC = 0, MHD_BC_OUTFLOW = 1 };
 enum { MHD_LIM_MINMOD = 0, MHD_LIM_MC = 1 };
 enum { MHD_RS_HLL = 0, MHD_RS_HLLD = 1 };
+enum { MHD_RK2 = 0, MHD_RK3 = 1 };
 
 /* Global grid. n[d] == 1 makes axis d inactive (1D uses x; 2D uses x, y).  Active axes
  * need n[d] >= 4.  lo < hi on every axis.  DESIGN.md §3.1. */
@@ -64,13 +65,14 @@ typedef struct {
   int32_t lo[3], hi[3];
 } mhd_bc;
 
-/* Scheme selection.  NULL => MC, HLLD, GLM on, alpha 0.1, floor 1e-12.
+/* Scheme selection.  NULL => MC, HLLD, GLM on, RK2, alpha 0.1, floor 1e-12.
  * GLM is required when two or more axes are active. */
 typedef struct {
   int32_t limiter;   /* MHD_LIM_* */
   int32_t riemann;   /* MHD_RS_* */
   int32_t glm;       /* 1: nvar = 9 with the psi field and c_h coupling */
-  int32_t reserved;
+  int32_t stepper;   /* MHD_RK2 (SSP-RK2, 2 stages, 2 state arrays) or MHD_RK3 (Shu-Osher
+                        SSP-RK3, the paper's integrator PAPER.md:179; 3 stages, 3 arrays) */
   double glm_alpha;  /* psi damping exp(-alpha*ch*dt/dx_min), R12 */
   double p_floor;    /* pressure floor on primitives (counted), R16 */
 } mhd_scheme;
@@ -97,7 +99,7 @@ typedef struct {
   int64_t plm_fallbacks;  /* (interior cell, direction, stage) first-order fallbacks */
   int64_t hlld_to_hll;    /* (face, stage) HLLD -> HLL fallbacks */
   int64_t first_bad_cell; /* lowest global interior linear index (z*ny+y)*nx+x, or -1 */
-  int32_t bad_stage;      /* 0 dt pass, 1/2 RK stage, -1 none */
+  int32_t bad_stage;      /* 0 dt pass or set_state, 1..3 RK stage, -1 none */
   int32_t reserved;
 } mhd_diag;
 
@@ -107,7 +109,7 @@ typedef struct mhd_ctx mhd_ctx; /* opaque; created by mhd_create, freed by mhd_d
 int mhd_nccl_get_unique_id(uint8_t out[128]);
 
 /* Validates the arguments (MHD_E_ARG), plans the slab, allocates the two padded state
- * arrays (U^n and U*) on the device and, for nranks > 1, creates the NCCL communicator
+ * arrays (U^n and U*; a third with MHD_RK3) on the device and, for nranks > 1, creates the NCCL communicator
  * (collective).  gamma > 1, 0 < cfl < 1.  *out receives the context (NULL on failure). */
 int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
                const mhd_scheme* scheme, const mhd_dist* dist, mhd_ctx** out);
@@ -137,7 +139,7 @@ int mhd_get_state(mhd_ctx* ctx, double* U, int32_t on_device);
  * preceding mhd_step.  Host-synchronising (16-byte read-back). */
 int mhd_compute_dt(mhd_ctx* ctx, double* dt);
 
-/* One SSP-RK2 step (rows a1-a5) with the given dt > 0 and the c_h cached
+/* One SSP-RK2 (or RK3) step (rows a1-a5) with the given dt > 0 and the c_h cached
  * by the last mhd_compute_dt on this state (recomputed if the state changed since).
  * Collective with nranks > 1; asynchronous with respect to the host.  Also produces the
  * partial maxima the next mhd_compute_dt needs. */

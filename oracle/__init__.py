@@ -35,7 +35,7 @@ class Config(C.Structure):
     _fields_ = [("n", C.c_int64 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
                 ("bc_lo", C.c_int32 * 3), ("bc_hi", C.c_int32 * 3), ("gamma", C.c_double),
                 ("cfl", C.c_double), ("limiter", C.c_int32), ("riemann", C.c_int32),
-                ("glm", C.c_int32), ("pad_", C.c_int32), ("glm_alpha", C.c_double),
+                ("glm", C.c_int32), ("stepper", C.c_int32), ("glm_alpha", C.c_double),
                 ("p_floor", C.c_double)]
 
 
@@ -104,6 +104,7 @@ def make_config(problem) -> Config:
     c.limiter = int(problem.limiter)
     c.riemann = int(problem.riemann)
     c.glm = int(problem.glm)
+    c.stepper = int(getattr(problem, "stepper", 0))
     c.glm_alpha = float(problem.glm_alpha)
     c.p_floor = float(problem.p_floor)
     return c

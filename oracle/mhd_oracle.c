@@ -604,7 +604,12 @@ int orc_stage(const orc_config* c, const double* U, double* Uout, double dt, dou
 }
 
 /* ------------------------------------------------------------------------ */
-/* c.11-c.12: one RK2 step (Heun / SSP-RK2) and the GLM damping               */
+/* c.11-c.12: one RK step and the GLM damping                                 */
+/*   SSP-RK2 (Heun, R2):  U* = S(U^n); U^{n+1} = 0.5 (U^n + S(U*))             */
+/*   SSP-RK3 (Shu & Osher 1988; the paper's integrator; reading  */
+/*   R30):  U1 = S(U^n); U2 = (3/4) U^n + (1/4) S(U1);                         */
+/*          U^{n+1} = (1/3) U^n + (2/3) S(U2), each as (a*U^n) + (b*S)          */
+/*   then psi^{n+1} <- psi^{n+1} * damp once per step (R12)                   */
 /* ------------------------------------------------------------------------ */
 int orc_step(const orc_config* c, double* U, double dt, double ch, orc_counters* cnt) {
   grid_t G;
@@ -612,6 +617,7 @@ int orc_step(const orc_config* c, double* U, double dt, double ch, orc_counters*
   if (rc) return rc;
   if (!(dt > 0.0) || !isfinite(dt)) return ORC_E_ARG;
   if (c->glm && !(ch > 0.0)) return ORC_E_ARG;
+  if (c->stepper != 0 && c->stepper != 1) return ORC_E_ARG;
   /* host scalars (R4) */
   double lam[3], dxmin = INFINITY;
   for (int d = 0; d < 3; ++d) {
@@ -622,26 +628,53 @@ int orc_step(const orc_config* c, double* U, double dt, double ch, orc_counters*
 
   const size_t np = padded_size(&G);
   double* Un = (double*)calloc(np, sizeof(double));
-  double* Us = (double*)calloc(np, sizeof(double));
-  double* Uss = (double*)calloc(np, sizeof(double));
+  double* Ua = (double*)calloc(np, sizeof(double));
+  double* Ub = (double*)calloc(np, sizeof(double));
   load_interior(&G, U, Un);
-  rc = stage_op(c, &G, Un, Us, lam, ch, 1, cnt); /* U* = S(U^n) */
-  if (rc == ORC_OK) rc = stage_op(c, &G, Us, Uss, lam, ch, 2, cnt); /* U** = S(U*) */
-  if (rc == ORC_OK) {
-    for (int f = 0; f < G.nvar; ++f)
-      for (int64_t k = 0; k < G.n[2]; ++k)
-        for (int64_t j = 0; j < G.n[1]; ++j)
-          for (int64_t i = 0; i < G.n[0]; ++i) {
-            const size_t q = P(&G, f, i, j, k);
-            double u = 0.5 * (Un[q] + Uss[q]); /* U^{n+1} = (U^n + U**)/2 */
-            if (f == 8) u = u * damp;          /* c.12 psi damping, once per step */
-            Uss[q] = u;
-          }
-    store_interior(&G, Uss, U);
+  rc = stage_op(c, &G, Un, Ua, lam, ch, 1, cnt); /* U* = S(U^n) */
+  if (rc == ORC_OK && c->stepper == 0) {
+    rc = stage_op(c, &G, Ua, Ub, lam, ch, 2, cnt); /* U** = S(U*) */
+    if (rc == ORC_OK) {
+      for (int f = 0; f < G.nvar; ++f)
+        for (int64_t k = 0; k < G.n[2]; ++k)
+          for (int64_t j = 0; j < G.n[1]; ++j)
+            for (int64_t i = 0; i < G.n[0]; ++i) {
+              const size_t q = P(&G, f, i, j, k);
+              double u = 0.5 * (Un[q] + Ub[q]); /* U^{n+1} = (U^n + U**)/2 */
+              if (f == 8) u = u * damp;         /* c.12 psi damping, once per step */
+              Ub[q] = u;
+            }
+      store_interior(&G, Ub, U);
+    }
+  } else if (rc == ORC_OK) {
+    const double a2 = 0.75, b2 = 0.25, a3 = 1.0 / 3.0, b3 = 2.0 / 3.0;
+    rc = stage_op(c, &G, Ua, Ub, lam, ch, 2, cnt); /* S(U1) */
+    if (rc == ORC_OK) {
+      for (int f = 0; f < G.nvar; ++f)
+        for (int64_t k = 0; k < G.n[2]; ++k)
+          for (int64_t j = 0; j < G.n[1]; ++j)
+            for (int64_t i = 0; i < G.n[0]; ++i) {
+              const size_t q = P(&G, f, i, j, k);
+              Ub[q] = (a2 * Un[q]) + (b2 * Ub[q]); /* U2 */
+            }
+      rc = stage_op(c, &G, Ub, Ua, lam, ch, 3, cnt); /* S(U2) */
+    }
+    if (rc == ORC_OK) {
+      for (int f = 0; f < G.nvar; ++f)
+        for (int64_t k = 0; k < G.n[2]; ++k)
+          for (int64_t j = 0; j < G.n[1]; ++j)
+            for (int64_t i = 0; i < G.n[0]; ++i) {
+              const size_t q = P(&G, f, i, j, k);
+              double u = (a3 * Un[q]) + (b3 * Ua[q]); /* U^{n+1} */
+              if (f == 8) u = u * damp;
+              Ua[q] = u;
+            }
+      store_interior(&G, Ua, U);
+    }
   }
   free(Un);
-  free(Us);
-  free(Uss);
+  free(Ua);
+  free(Ub);
   return rc;
 }
 

@@ -36,7 +36,7 @@ typedef struct {
   int32_t limiter;     /* 0 minmod, 1 MC (R? c.5) */
   int32_t riemann;     /* 0 HLL, 1 HLLD */
   int32_t glm;         /* 1 => 9 fields with GLM cleaning */
-  int32_t pad_;
+  int32_t stepper;     /* 0 SSP-RK2 (Heun, R2), 1 SSP-RK3 (Shu-Osher) */
   double glm_alpha;    /* 0.1 (R12) */
   double p_floor;      /* 1e-12 (R16) */
 } orc_config;
@@ -46,7 +46,7 @@ typedef struct {
   int64_t plm_fallbacks; /* per (interior cell, active direction, stage) */
   int64_t hlld_to_hll;   /* per (face, stage) */
   int64_t first_bad_cell;/* lowest interior linear index (z*ny+y)*nx+x, or -1 */
-  int32_t bad_stage;     /* 0 = dt pass, 1/2 = RK stage; -1 none */
+  int32_t bad_stage;     /* 0 = dt pass, 1..3 = RK stage; -1 none */
   int32_t pad_;
 } orc_counters;
 

@@ -39,10 +39,11 @@ struct mhd_ctx {
   int up, down;  // ring neighbours along z (-1: none)
   // device state
   double* U0 = nullptr;  // U^n
-  double* U1 = nullptr;  // U*
+  double* U1 = nullptr;  // U* (RK2) / U1 (RK3)
+  double* U2 = nullptr;  // RK3 only: U2
   size_t arr_elems = 0;
-  unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..7] bad slots, [16] debug
-  unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (same 8 entries)
+  unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..8] bad slots, [20] debug
+  unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (the first 9 entries)
   unsigned long long* hbuf = nullptr;  // pinned host mirror
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -118,6 +119,45 @@ StageConsts make_consts(const mhd_ctx* c, double dt, double ch) {
   return k;
 }
 
+// the arrays and epilogue of RK stage `stage` (1-based) of the context's stepper (§3.11):
+// RK2: S(U^n) -> U1;  0.5 (U^n + S(U1)) -> U^n
+// RK3: S(U^n) -> U1;  (3/4) U^n + (1/4) S(U1) -> U2;  (1/3) U^n + (2/3) S(U2) -> U^n
+struct StagePlan {
+  double* in;
+  double* out;
+  int mode;
+  double wa, wb;
+  int last;
+};
+int nstages(const mhd_ctx* c) { return c->scheme.stepper == MHD_RK3 ? 3 : 2; }
+StagePlan stage_plan(const mhd_ctx* c, int stage) {
+  StagePlan p;
+  p.wa = p.wb = 0.0;
+  if (stage == 1) {
+    p.in = c->U0;
+    p.out = c->U1;
+    p.mode = 0;
+  } else if (c->scheme.stepper != MHD_RK3) {
+    p.in = c->U1;
+    p.out = c->U0;
+    p.mode = 1;
+  } else if (stage == 2) {
+    p.in = c->U1;
+    p.out = c->U2;
+    p.mode = 2;
+    p.wa = 0.75;
+    p.wb = 0.25;
+  } else {
+    p.in = c->U2;
+    p.out = c->U0;
+    p.mode = 2;
+    p.wa = 1.0 / 3.0;
+    p.wb = 2.0 / 3.0;
+  }
+  p.last = stage == nstages(c);
+  return p;
+}
+
 // a1 (z part).  Halo plan of one stage for a z slab: the transfers in posting order as
 // (peer, 0 send / 1 recv, first storage plane, planes).  Storage planes: 0,1 bottom ghosts,
 // 2..nz+1 interior, nz+2, nz+3 top ghosts.  Sends: top 2 interior planes -> up, bottom 2
@@ -184,16 +224,16 @@ int exchange_nccl(mhd_ctx* c, double* U) {
 
 // exchange part for an in-process group: receives are device copies from the peer slab's
 // array (the same array role: U^n or U*)
-int exchange_local(mhd_ctx* c, int which) {
+int exchange_local(mhd_ctx* c, int stage) {
   const size_t pe = plane_elems(c), pb = pe * sizeof(double);
   int plan[4][4];
   if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, plan))
     return set_err(c, MHD_E_ARG, "halo plan");
-  double* mine = which == 0 ? c->U0 : c->U1;
+  double* mine = stage_plan(c, stage).in;
   for (int i = 0; i < 4; ++i) {
     if (plan[i][0] < 0 || plan[i][1] != 1) continue;  // receives only
     const mhd_ctx* peer = c->group[plan[i][0]];
-    const double* theirs = which == 0 ? peer->U0 : peer->U1;
+    const double* theirs = stage_plan(peer, stage).in;
     // the peer sends its top interior planes to its up neighbour, bottom ones to its down
     // neighbour: my bottom ghosts (recv from down) <- down's storage planes nz, nz+1;
     // my top ghosts (recv from up) <- up's storage planes 2, 3
@@ -233,10 +273,15 @@ void prof_drain(mhd_ctx* c) {
 }
 
 int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
+  const StagePlan sp = stage_plan(c, stage);
   StageArgs a;
-  a.Uin = stage == 1 ? c->U0 : c->U1;
+  a.Uin = sp.in;
   a.Un = c->U0;
-  a.Uout = stage == 1 ? c->U1 : c->U0;
+  a.Uout = sp.out;
+  a.mode = sp.mode;
+  a.wa = sp.wa;
+  a.wb = sp.wb;
+  a.last = sp.last;
   a.nx = c->nx;
   a.ny = c->ny;
   a.nz_loc = c->nzl;
@@ -289,17 +334,17 @@ int reduce_and_read(mhd_ctx* c) {
     NCCL_OR_RETURN(c, ncclGroupStart());
     NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf, c->dred, 2, ncclUint64, ncclMax, c->comm, c->stream));
     NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf + 2, c->dred + 2, 3, ncclUint64, ncclSum, c->comm, c->stream));
-    NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf + 5, c->dred + 5, 3, ncclUint64, ncclMin, c->comm, c->stream));
+    NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf + 5, c->dred + 5, 4, ncclUint64, ncclMin, c->comm, c->stream));
     NCCL_OR_RETURN(c, ncclGroupEnd());
     src = c->dred;
   }
-  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf, src, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf, src, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
   c->diag.p_floors = (int64_t)c->hbuf[2];
   c->diag.plm_fallbacks = (int64_t)c->hbuf[3];
   c->diag.hlld_to_hll = (int64_t)c->hbuf[4];
   // time order of the records: stage 1 and stage 2 of the last step, then the dt pass
-  for (int s : {1, 2, 0}) {
+  for (int s : {1, 2, 3, 0}) {
     if (c->hbuf[5 + s] != ~0ULL) {
       c->diag.bad_stage = s;
       c->diag.first_bad_cell = (int64_t)c->hbuf[5 + s];
@@ -311,7 +356,7 @@ int reduce_and_read(mhd_ctx* c) {
 
 int reset_device_records(mhd_ctx* c) {
   CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 5 * sizeof(unsigned long long), c->stream));
-  CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf + 5, 0xff, 3 * sizeof(unsigned long long), c->stream));
+  CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf + 5, 0xff, 4 * sizeof(unsigned long long), c->stream));
   return MHD_OK;
 }
 
@@ -378,12 +423,13 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     c->scheme.limiter = MHD_LIM_MC;
     c->scheme.riemann = MHD_RS_HLLD;
     c->scheme.glm = 1;
-    c->scheme.reserved = 0;
+    c->scheme.stepper = MHD_RK2;
     c->scheme.glm_alpha = 0.1;
     c->scheme.p_floor = 1e-12;
   }
   if ((c->scheme.limiter != MHD_LIM_MINMOD && c->scheme.limiter != MHD_LIM_MC) ||
       (c->scheme.riemann != MHD_RS_HLL && c->scheme.riemann != MHD_RS_HLLD) || (c->scheme.glm != 0 && c->scheme.glm != 1) ||
+      (c->scheme.stepper != MHD_RK2 && c->scheme.stepper != MHD_RK3) ||
       !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm)) {
     delete c;
     return MHD_E_ARG;
@@ -446,12 +492,14 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   cudaError_t e1 = cudaMalloc(&c->U0, c->arr_elems * sizeof(double));
   cudaError_t e2 = cudaMalloc(&c->U1, c->arr_elems * sizeof(double));
   cudaError_t e3 = cudaMalloc(&c->dbuf, 24 * sizeof(unsigned long long));
+  if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.stepper == MHD_RK3)
+    e2 = cudaMalloc(&c->U2, c->arr_elems * sizeof(double));
   cudaError_t e4 = cudaMallocHost(&c->hbuf, 24 * sizeof(unsigned long long));
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
     mhd_destroy(c);
     return MHD_E_NOMEM;
   }
-  c->dred = c->dbuf + 8;
+  c->dred = c->dbuf + 9;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
     mhd_destroy(c);
     return MHD_E_CUDA;
@@ -460,6 +508,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   // zero the arrays so ghost planes never hold garbage
   cudaMemsetAsync(c->U0, 0, c->arr_elems * sizeof(double), c->stream);
   cudaMemsetAsync(c->U1, 0, c->arr_elems * sizeof(double), c->stream);
+  if (c->U2) cudaMemsetAsync(c->U2, 0, c->arr_elems * sizeof(double), c->stream);
   if (reset_device_records(c) != MHD_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) {
     mhd_destroy(c);
     return MHD_E_CUDA;
@@ -508,7 +557,7 @@ int mhd_local_box(const mhd_ctx* c, int64_t off[3], int64_t ext[3]) {
 
 int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
   if (!c || !bytes) return MHD_E_ARG;
-  *bytes = 2 * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
+  *bytes = (c->U2 ? 3 : 2) * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
   return MHD_OK;
 }
 
@@ -597,8 +646,8 @@ int mhd_step(mhd_ctx* c, double dt) {
   }
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
-  for (int stage = 1; stage <= 2; ++stage) {
-    double* U = stage == 1 ? c->U0 : c->U1;
+  for (int stage = 1; stage <= nstages(c); ++stage) {
+    double* U = stage_plan(c, stage).in;
     if ((rc = fill_z_ghosts_local(c, U))) return rc;
     if (c->nranks > 1 && c->dim == 3) {
       // halo exchange on the comm stream, overlapped with the interior planes [2, nz-2)
@@ -673,11 +722,11 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
   if (!(dt > 0.0) || !std::isfinite(dt)) return MHD_E_ARG;
   for (int r = 0; r < n; ++r)
     if (!ctxs[r]->ch_valid) return set_err(ctxs[r], MHD_E_STATE, "call mhd_group_compute_dt first");
-  for (int stage = 1; stage <= 2; ++stage) {
+  for (int stage = 1; stage <= nstages(ctxs[0]); ++stage) {
     for (int r = 0; r < n; ++r) {
       mhd_ctx* c = ctxs[r];
-      if ((rc = fill_z_ghosts_local(c, stage == 1 ? c->U0 : c->U1))) return rc;
-      if (n > 1 && (rc = exchange_local(c, stage == 1 ? 0 : 1))) return rc;
+      if ((rc = fill_z_ghosts_local(c, stage_plan(c, stage).in))) return rc;
+      if (n > 1 && (rc = exchange_local(c, stage))) return rc;
     }
     for (int r = 0; r < n; ++r) {
       mhd_ctx* c = ctxs[r];
@@ -709,6 +758,7 @@ void mhd_destroy(mhd_ctx* c) {
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   if (c->U0) cudaFree(c->U0);
   if (c->U1) cudaFree(c->U1);
+  if (c->U2) cudaFree(c->U2);
   if (c->dbuf) cudaFree(c->dbuf);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -743,13 +793,13 @@ int mhd_debug_face_flux(mhd_ctx* c, const double* VL, const double* VR, int64_t 
     return MHD_OK;
   }
   const StageConsts k = make_consts(c, 1.0, ch);
-  unsigned long long* cnt = c->dbuf + 16;
+  unsigned long long* cnt = c->dbuf + 20;
   CUDA_OR_RETURN(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream));
   cudaError_t e = mhd::launch_face_flux(c->nv, c->scheme.riemann, VL, VR, n, k, F, cnt, c->stream);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "face flux: %s", cudaGetErrorString(e));
-  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 16, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 20, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
-  if (n_hll) *n_hll = (int64_t)c->hbuf[16];
+  if (n_hll) *n_hll = (int64_t)c->hbuf[20];
   return MHD_OK;
 }
 

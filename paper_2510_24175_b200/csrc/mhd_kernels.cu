@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
       for (int f = 0; f < NV; ++f) {
         prefetch_l2(a.Uin + plane_off(k + 3 < nzl + a.gz ? k + 3 : k) + f * fstride + own_cell);
         prefetch_l1(a.Uin + plane_off(k + 2) + f * fstride + own_cell);
-        if (full && a.stage == 2) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
+        if (full && a.mode != 0) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
       }
     }
 #pragma unroll 1
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
         u0[f] = __ldg(a.Uin + off + f * fstride);
-        un[f] = (a.stage == 2) ? a.Un[off + f * fstride] : 0.0;
+        un[f] = (a.mode != 0) ? a.Un[off + f * fstride] : 0.0;
       }
     }
     __syncthreads();
@@ -359,13 +359,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
         if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
         if constexpr (DIM == 3) r = r + c.lam[2] * (fzn[f * NC + tid] - fzo[f * NC + tid]);
         const double s = u0[f] - r;
-        if (a.stage == 1) {
-          a.Uout[off + f * fstride] = s;
-        } else {
-          double v = 0.5 * (un[f] + s);  // U^{n+1} = (U^n + U**)/2
-          if (NV > 8 && f == NV - 1) v = v * c.damp;
-          a.Uout[off + f * fstride] = v;
-        }
+        double v = s;
+        if (a.mode == 1) v = 0.5 * (un[f] + s);                    // RK2: U^{n+1} = (U^n + U**)/2
+        else if (a.mode == 2) v = (a.wa * un[f]) + (a.wb * s);     // RK3: (a U^n) + (b S(U))
+        if (NV > 8 && f == NV - 1 && a.last) v = v * c.damp;       // GLM damping once per step
+        a.Uout[off + f * fstride] = v;
       }
     }
     // ---- advance the plane window (3D)

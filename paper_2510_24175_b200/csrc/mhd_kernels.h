@@ -21,10 +21,13 @@ struct StageArgs {
   int bcx[2], bcy[2]; // 0 periodic, 1 outflow
   int kz;             // z planes per CTA
   int zb, ze;         // local z range of cells this launch updates (interior/boundary split)
-  int stage;          // 1 or 2
+  int stage;          // 1, 2 (, 3): selects the bad-cell slot
+  int mode;           // epilogue: 0 S(U); 1 0.5 (U^n + S) (RK2); 2 (a U^n) + (b S) (RK3)
+  int last;           // last stage of the step: apply the GLM damping
+  double wa, wb;      // RK3 weights a, b
   StageConsts c;
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
-  unsigned long long* bad;       // [3] lowest bad global linear index per stage (0 = dt pass)
+  unsigned long long* bad;       // [4] lowest bad global linear index per stage (0 = dt pass)
 };
 
 struct DtArgs {

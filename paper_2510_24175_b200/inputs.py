@@ -27,6 +27,7 @@ from typing import Tuple
 import numpy as np
 
 PERIODIC, OUTFLOW = 0, 1
+RK2, RK3 = 0, 1
 MINMOD, MC = 0, 1
 HLL, HLLD = 0, 1
 
@@ -46,6 +47,7 @@ class Problem:
     glm_alpha: float = 0.1
     p_floor: float = 1e-12
     t_end: float = 0.0
+    stepper: int = 0  # 0 SSP-RK2 (north star), 1 SSP-RK3 (the paper's RK3)
 
     @property
     def nvar(self) -> int:

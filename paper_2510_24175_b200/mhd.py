@@ -41,7 +41,7 @@ class BC(C.Structure):
 
 
 class Scheme(C.Structure):
-    _fields_ = [("limiter", C.c_int32), ("riemann", C.c_int32), ("glm", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("limiter", C.c_int32), ("riemann", C.c_int32), ("glm", C.c_int32), ("stepper", C.c_int32),
                 ("glm_alpha", C.c_double), ("p_floor", C.c_double)]
 
 
@@ -154,8 +154,8 @@ class Solver:
             g.hi[d] = float(problem.hi[d])
             bc.lo[d] = int(problem.bc[d])
             bc.hi[d] = int(problem.bc[d])
-        sc = Scheme(int(problem.limiter), int(problem.riemann), int(problem.glm), 0, float(problem.glm_alpha),
-                    float(problem.p_floor))
+        sc = Scheme(int(problem.limiter), int(problem.riemann), int(problem.glm), int(getattr(problem, "stepper", 0)),
+                    float(problem.glm_alpha), float(problem.p_floor))
         dist = None
         if nranks > 1 or device >= 0:
             dist = Dist(rank, nranks, device, transport)

@@ -307,3 +307,40 @@ def test_cpa3d_full_period(mhd):
     p = I.cpa_3d(24)
     res = run_both(mhd, p, I.cpa_3d_ic(p), 10 ** 6, p.t_end)
     assert_parity(*res)
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) row 2: SSP-RK3 (the paper's integrator), three state arrays
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["ot3d", "brio_wu", "ot2d"])
+def test_rk3_parity(mhd, case):
+    if case == "ot3d":
+        p = I.orszag_tang_3d(32).replace(n=(40, 21, 19), hi=(1.25, 0.65625, 0.59375), stepper=I.RK3)
+        U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+        n = 10
+    elif case == "brio_wu":
+        p = I.brio_wu(512).replace(stepper=I.RK3)
+        U0 = I.brio_wu_ic(p)
+        n = 100000
+    else:
+        p = I.orszag_tang_2d(64).replace(stepper=I.RK3)
+        U0 = I.orszag_tang_2d_ic(p)
+        n = 60
+    res = run_both(mhd, p, U0, n, p.t_end if case == "brio_wu" else 0.0)
+    assert_parity(*res)
+
+
+def test_rk3_slab_group_bitwise(mhd):
+    p = I.orszag_tang_3d(32).replace(stepper=I.RK3)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(5)
+    U1 = s.get_state()
+    s.destroy()
+    g = mhd.SolverGroup(p, 4)
+    g.set_state(U0)
+    log4 = g.run(5)
+    U4 = g.get_state()
+    g.destroy()
+    assert np.array_equal(log1, log4) and np.array_equal(U1, U4)

@@ -265,3 +265,36 @@ def test_cpa_3d_exact_solution_definition():
     assert np.allclose(Bpar, 1.0, atol=1e-14)
     bperp2 = sum(B0[c] ** 2 for c in range(3)) - Bpar ** 2
     assert np.allclose(bperp2, 0.01, atol=1e-14)
+
+
+@pytest.mark.parametrize("stepper,order", [(I.RK2, 2.0), (I.RK3, 3.0)])
+def test_time_integrator_order(stepper, order):
+    """§8(f) row 2 (SSP-RK3, the paper's integrator) and R2 (SSP-RK2): temporal
+    self-convergence on a fixed grid.  A smooth monotone density ramp advected at v = 1 keeps the
+    MC limiter on its central branch (the semi-discrete system is linear), so the difference to a
+    CFL/32 reference falls as dt^order (a wrong stage weight drops RK3 to first or second order)."""
+    def run(cfl):
+        p = I.Problem("adv", (128, 1, 1), bc=(I.OUTFLOW,) * 3, gamma=1.4, glm=0, riemann=I.HLLD, cfl=cfl,
+                      stepper=stepper)
+        X, _, _ = I.mesh(p)
+        U = I.prim_to_cons_ic(p, 1 + 0.2 * np.tanh((X - 0.4) / 0.15), 1.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0)
+        o = oracle.Oracle(p, U)
+        o.run(10 ** 6, 0.1)
+        return o.U[0, 0, 0].copy()
+    ref = run(0.4 / 32)
+    e = [np.abs(run(c) - ref).max() for c in (0.4, 0.2, 0.1)]
+    orders = [math.log2(e[i] / e[i + 1]) for i in range(2)]
+    assert all(abs(o - order) < 0.4 for o in orders), (e, orders)
+
+
+def test_rk3_uniform_state_and_damping():
+    """RK3 on a uniform periodic state: flux differences vanish, so every stage is
+    U2 = 0.75 U + 0.25 U and U^{n+1} = U/3 + 2U/3 (exact to 1 ulp); psi decays by damp once."""
+    p = I.orszag_tang_3d(8).replace(stepper=I.RK3)
+    U = I.prim_to_cons_ic(p, 1.3, 0.2, -0.1, 0.3, 0.7, 0.4, 0.5, -0.6, psi=0.05)
+    o = oracle.Oracle(p, U)
+    dt, ch = o.compute_dt()
+    o.step(dt, ch)
+    assert np.allclose(o.U[:8], U[:8], rtol=2.3e-16, atol=0)
+    damp = math.exp(-(0.1 * ch * dt) / (1.0 / 8))
+    assert np.allclose(o.U[8], 0.05 * damp, rtol=5e-16, atol=0)
