@@ -66,6 +66,8 @@ def lib():
         L.orc_fast_speed.restype = C.c_double
         L.orc_limited_slope.argtypes = [C.c_int32, C.c_double, C.c_double]
         L.orc_limited_slope.restype = C.c_double
+        L.orc_wenoz.argtypes = [C.c_double] * 5
+        L.orc_wenoz.restype = C.c_double
         L.orc_face_flux.argtypes = [C.POINTER(Config), _D, _D, C.c_double, _D]
         L.orc_face_flux.restype = C.c_int
         L.orc_face_flux_batch.argtypes = [C.POINTER(Config), _D, _D, C.c_int64, C.c_double, _D]
@@ -173,6 +175,10 @@ def total_energy(gamma, V):
 
 def fast_speed(gamma, rho, p, bn, bt1, bt2):
     return lib().orc_fast_speed(gamma, rho, p, bn, bt1, bt2)
+
+
+def wenoz(a, b, c, d, e):
+    return lib().orc_wenoz(a, b, c, d, e)
 
 
 def limited_slope(limiter, dm, dp):

@@ -52,13 +52,14 @@ typedef struct {
 static int make_grid(const orc_config* c, grid_t* G) {
   if (!c) return ORC_E_ARG;
   if (!(c->gamma > 1.0) || !(c->cfl > 0.0 && c->cfl < 1.0)) return ORC_E_ARG;
+  if (c->limiter < 0 || c->limiter > 2) return ORC_E_ARG;
   int nact = 0;
   for (int d = 0; d < 3; ++d) {
     if (c->n[d] < 1) return ORC_E_ARG;
     G->n[d] = c->n[d];
     G->act[d] = c->n[d] > 1;
     if (G->act[d] && c->n[d] < 4) return ORC_E_ARG;
-    G->g[d] = G->act[d] ? 2 : 0;
+    G->g[d] = G->act[d] ? (c->limiter == 2 ? 3 : 2) : 0; /* PLM 2, WENOZ 3 (R19) */
     G->m[d] = G->n[d] + 2 * G->g[d];
     if (!(c->hi[d] > c->lo[d])) return ORC_E_ARG;
     G->dx[d] = (c->hi[d] - c->lo[d]) / (double)c->n[d];
@@ -96,12 +97,12 @@ static void store_interior(const grid_t* G, const double* Up, double* U) {
 }
 
 /* ------------------------------------------------------------------------ */
-/* c.2 ghost fill (row a1): periodic wrap or zero-gradient outflow, 2 cells   */
+/* c.2 ghost fill (row a1): periodic wrap or zero-gradient outflow, g cells   */
 /* ------------------------------------------------------------------------ */
 static void fill_ghosts(const orc_config* c, const grid_t* G, double* Up) {
   for (int d = 0; d < 3; ++d) {
     if (!G->act[d]) continue;
-    const int64_t N = G->n[d];
+    const int64_t N = G->n[d], g = G->g[d];
     /* the two other axes, interior range (edge/corner ghosts are never read) */
     const int a = (d + 1) % 3, b = (d + 2) % 3;
     for (int f = 0; f < G->nvar; ++f)
@@ -111,27 +112,39 @@ static void fill_ghosts(const orc_config* c, const grid_t* G, double* Up) {
           idx[a] = r;
           idx[b] = q;
 #define AT(s) (*(idx[d] = (s), &Up[P(G, f, idx[0], idx[1], idx[2])]))
-          if (c->bc_lo[d] == 0) { /* periodic: U[-1]=U[N-1], U[-2]=U[N-2] */
-            double v1 = AT(N - 1), v2 = AT(N - 2);
-            AT(-1) = v1;
-            AT(-2) = v2;
-          } else { /* outflow: U[-2]=U[-1]=U[0] */
-            double v0 = AT(0);
-            AT(-1) = v0;
-            AT(-2) = v0;
-          }
-          if (c->bc_hi[d] == 0) { /* periodic: U[N]=U[0], U[N+1]=U[1] */
-            double v0 = AT(0), v1 = AT(1);
-            AT(N) = v0;
-            AT(N + 1) = v1;
-          } else { /* outflow: U[N]=U[N+1]=U[N-1] */
-            double vl = AT(N - 1);
-            AT(N) = vl;
-            AT(N + 1) = vl;
+          for (int64_t m = 1; m <= g; ++m) {
+            /* periodic: U[-m] = U[N-m], U[N-1+m] = U[m-1]; outflow: U[-m] = U[0], U[N-1+m] = U[N-1] */
+            const double lo_src = (c->bc_lo[d] == 0) ? AT(N - m) : AT(0);
+            AT(-m) = lo_src;
+            const double hi_src = (c->bc_hi[d] == 0) ? AT(m - 1) : AT(N - 1);
+            AT(N - 1 + m) = hi_src;
           }
 #undef AT
         }
   }
+}
+
+/* ------------------------------------------------------------------------ */
+/* WENO-Z reconstruction (the paper's scheme; */
+/* Borges, Carmona, Costa & Don 2008 with the Jiang-Shu smoothness indicators; */
+/* reading R31: eps = 1e-40, p = 2, linear weights 1/10, 6/10, 3/10).  The     */
+/* value at the face between c and d from the 5 cells (a, b, c, d, e):         */
+/* ------------------------------------------------------------------------ */
+double orc_wenoz(double a, double b, double c, double d, double e) {
+  const double eps = 1e-40;
+  const double t0 = (a - 2.0 * b) + c, u0 = (a - 4.0 * b) + 3.0 * c;
+  const double t1 = (b - 2.0 * c) + d, u1 = b - d;
+  const double t2 = (c - 2.0 * d) + e, u2 = (3.0 * c - 4.0 * d) + e;
+  const double b0 = (13.0 / 12.0) * (t0 * t0) + 0.25 * (u0 * u0);
+  const double b1 = (13.0 / 12.0) * (t1 * t1) + 0.25 * (u1 * u1);
+  const double b2 = (13.0 / 12.0) * (t2 * t2) + 0.25 * (u2 * u2);
+  const double tau = fabs(b0 - b2);
+  const double r0 = tau / (b0 + eps), r1 = tau / (b1 + eps), r2 = tau / (b2 + eps);
+  const double a0 = 0.1 * (1.0 + r0 * r0), a1 = 0.6 * (1.0 + r1 * r1), a2 = 0.3 * (1.0 + r2 * r2);
+  const double p0 = (2.0 * a - 7.0 * b) + 11.0 * c; /* 6 x the candidate values */
+  const double p1 = (5.0 * c - b) + 2.0 * d;
+  const double p2 = (2.0 * c + 5.0 * d) - e;
+  return ((a0 * p0 + a1 * p1) + a2 * p2) / (6.0 * ((a0 + a1) + a2));
 }
 
 /* ------------------------------------------------------------------------ */
@@ -442,6 +455,7 @@ static void from_normal(int d, int nvar, const double* W, double* V) {
 /* interior written.                                                          */
 /* ------------------------------------------------------------------------ */
 static int in_star(const grid_t* G, int64_t i, int64_t j, int64_t k) {
+  /* every padded cell within the ghost width of the interior along at most one axis */
   int outside = (i < 0 || i >= G->n[0]) + (j < 0 || j >= G->n[1]) + (k < 0 || k >= G->n[2]);
   return outside <= 1;
 }
@@ -499,7 +513,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
     F[d] = (double*)calloc(np, sizeof(double));
     int64_t off[3] = {0, 0, 0};
     off[d] = 1;
-    /* PLM for cells -1..N along d, interior along the other axes */
+    /* reconstruction for cells -1..N along d, interior along the other axes */
     int64_t lo3[3] = {0, 0, 0}, hi3[3] = {G->n[0], G->n[1], G->n[2]};
     lo3[d] = -1;
     hi3[d] = G->n[d] + 1;
@@ -512,11 +526,18 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
             const double qa = V[P(G, f, i - off[0], j - off[1], k - off[2])];
             const double qb = V[P(G, f, i, j, k)];
             const double qc = V[P(G, f, i + off[0], j + off[1], k + off[2])];
-            const double dm = qb - qa, dp = qc - qb;
-            const double s = orc_limited_slope(c->limiter, dm, dp);
             q0[f] = qb;
-            qp[f] = qb + 0.5 * s;
-            qm[f] = qb - 0.5 * s;
+            if (c->limiter == 2) { /* WENOZ: q+ from (i-2..i+2), q- from the mirrored stencil */
+              const double qaa = V[P(G, f, i - 2 * off[0], j - 2 * off[1], k - 2 * off[2])];
+              const double qcc = V[P(G, f, i + 2 * off[0], j + 2 * off[1], k + 2 * off[2])];
+              qp[f] = orc_wenoz(qaa, qa, qb, qc, qcc);
+              qm[f] = orc_wenoz(qcc, qc, qb, qa, qaa);
+            } else { /* PLM (c.5) */
+              const double dm = qb - qa, dp = qc - qb;
+              const double s = orc_limited_slope(c->limiter, dm, dp);
+              qp[f] = qb + 0.5 * s;
+              qm[f] = qb - 0.5 * s;
+            }
           }
           if (!(qp[0] > 0.0 && qm[0] > 0.0 && qp[4] > 0.0 && qm[4] > 0.0)) { /* positivity fallback (R17) */
             for (int f = 0; f < nvar; ++f) qp[f] = qm[f] = q0[f];

@@ -33,7 +33,7 @@ typedef struct {
   double lo[3], hi[3]; /* domain extent */
   int32_t bc_lo[3], bc_hi[3]; /* 0 periodic, 1 outflow (R18) */
   double gamma, cfl;
-  int32_t limiter;     /* 0 minmod, 1 MC (R? c.5) */
+  int32_t limiter;     /* 0 minmod, 1 MC (c.5), 2 WENOZ (R31; ghost width 3) */
   int32_t riemann;     /* 0 HLL, 1 HLLD */
   int32_t glm;         /* 1 => 9 fields with GLM cleaning */
   int32_t stepper;     /* 0 SSP-RK2 (Heun, R2), 1 SSP-RK3 (Shu-Osher) */
@@ -58,6 +58,8 @@ int orc_cons2prim(const orc_config* c, const double* U, double* V);
 double orc_total_energy(double gamma, const double* V);
 /* c.4 fast magnetosonic speed. */
 double orc_fast_speed(double gamma, double rho, double p, double bn, double bt1, double bt2);
+/* WENO-Z face value between c and d from the cells (a, b, c, d, e) (R31). */
+double orc_wenoz(double a, double b, double c, double d, double e);
 /* c.5 limited slope. */
 double orc_limited_slope(int32_t limiter, double dm, double dp);
 /* c.6-c.10: one face flux in the normal frame (rho,vn,vt1,vt2,p,Bn,Bt1,Bt2[,psi]).

@@ -28,7 +28,7 @@ import numpy as np
 
 PERIODIC, OUTFLOW = 0, 1
 RK2, RK3 = 0, 1
-MINMOD, MC = 0, 1
+MINMOD, MC, WENOZ = 0, 1, 2
 HLL, HLLD = 0, 1
 
 

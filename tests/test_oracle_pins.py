@@ -319,3 +319,49 @@ def test_frame_rotation_invariance_bitwise():
                 src = 5 + (f - 5 - d) % 3
             assert np.array_equal(out_d[f].ravel(), out_x[src].ravel()), (d, f)
         assert cd == cx
+
+
+# ---------------------------------------------------------------------------------------------
+# WENO-Z reconstruction (§8(f) row 3; Borges et al. 2008, reading R31)
+# ---------------------------------------------------------------------------------------------
+def test_wenoz_constants_and_quadratics():
+    for c in (1.0, 1.3, -2.7e-3, 5e4):
+        assert abs(oracle.wenoz(c, c, c, c, c) - c) <= 4 * np.finfo(float).eps * abs(c)
+    # cell averages of a quadratic: all three candidate stencils are exact, so the face value
+    # is exact whatever the nonlinear weights (f = x^2 on unit cells: avg_i = i^2 + 1/12)
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        a2, a1, a0, h = rng.normal(size=3).tolist() + [10 ** rng.uniform(-3, 0)]
+        def avg(i):  # average of a0 + a1 x + a2 x^2 over [(i-1/2)h, (i+1/2)h]
+            return a0 + a1 * i * h + a2 * (i * i * h * h + h * h / 12.0)
+        exact = a0 + a1 * 0.5 * h + a2 * 0.25 * h * h
+        got = oracle.wenoz(avg(-2), avg(-1), avg(0), avg(1), avg(2))
+        scale = abs(a0) + abs(a1) + abs(a2)
+        assert abs(got - exact) <= 1e-13 * scale
+
+
+def test_wenoz_essentially_non_oscillatory():
+    """a jump across the face: the upwind smooth stencil dominates (weights of the stencils that
+    cross the jump vanish like eps^2/beta^2), so no overshoot."""
+    assert abs(oracle.wenoz(0.0, 0.0, 0.0, 1.0, 1.0)) < 1e-30
+    assert abs(oracle.wenoz(1.0, 1.0, 0.0, 0.0, 0.0)) < 1e-30
+    rng = np.random.default_rng(5)
+    for _ in range(500):
+        lo, hi = sorted(rng.normal(size=2))
+        v = [lo, lo, lo, hi, hi]
+        q = oracle.wenoz(*v)
+        assert lo - 1e-12 <= q <= lo + 1e-6 * (hi - lo) + 1e-12
+
+
+def test_wenoz_fifth_order_on_smooth_data():
+    """on smooth data the WENO-Z weights approach the linear weights fast enough that the
+    reconstruction error of cell averages of sin falls at >= 4th order (5th for linear weights)."""
+    errs = []
+    for h in (0.1, 0.05, 0.025):
+        def avg(i):  # average of sin over [(i-1/2)h + x0, (i+1/2)h + x0]
+            x0 = 0.3
+            return (math.cos(x0 + (i - 0.5) * h) - math.cos(x0 + (i + 0.5) * h)) / h
+        got = oracle.wenoz(avg(-2), avg(-1), avg(0), avg(1), avg(2))
+        errs.append(abs(got - math.sin(0.3 + 0.5 * h)))
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert min(orders) >= 4.0, (errs, orders)

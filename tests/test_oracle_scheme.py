@@ -298,3 +298,55 @@ def test_rk3_uniform_state_and_damping():
     assert np.allclose(o.U[:8], U[:8], rtol=2.3e-16, atol=0)
     damp = math.exp(-(0.1 * ch * dt) / (1.0 / 8))
     assert np.allclose(o.U[8], 0.05 * damp, rtol=5e-16, atol=0)
+
+
+@pytest.mark.parametrize("stepper,order_min", [(I.RK3, 2.9), (I.RK2, 1.95)])
+def test_wenoz_cpa_convergence(stepper, order_min):
+    """WENOZ (the paper's reconstruction) with RK3 converges at the integrator's
+    third order on the exact CPA solution (RK2: second), with errors far below PLM's."""
+    errs = []
+    for n in (32, 64, 128):
+        p = I.cpa_1d(n, limiter=I.WENOZ).replace(stepper=stepper)
+        U0 = I.cpa_1d_ic(p)
+        o = oracle.Oracle(p, U0)
+        o.run(10 ** 6, p.t_end)
+        errs.append(np.abs(o.U[6] - U0[6]).mean() / 0.1)
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert orders[-1] >= order_min, (errs, orders)
+    if stepper == I.RK3:
+        assert errs[-1] < 2e-6
+
+
+def test_wenoz_sod_plateaus():
+    g = json.load(open(os.path.join(GOLD, "sod_toro_test1.json")))
+    p = I.sod(512).replace(limiter=I.WENOZ, stepper=I.RK3)
+    o = oracle.Oracle(p, I.sod_ic(p))
+    o.run(100000, p.t_end)
+    r, v, pr, _ = prims(p, o.U)
+    for xx in (0.56, 0.60, 0.64):
+        assert abs(r[0, 0, int(xx * 512)] - g["rho_star_left"]) < 1e-3
+        assert abs(pr[0, 0, int(xx * 512)] - g["p_star"]) < 1e-3
+    for xx in (0.74, 0.78, 0.81):
+        assert abs(r[0, 0, int(xx * 512)] - g["rho_star_right"]) < 2e-3
+
+
+def test_wenoz_3d_ot_conservation_and_embedding():
+    """3D WENOZ path: periodic conservation to round-off, and a 1D problem embedded in 3D gives
+    the 1D result bitwise (ghost width 3 along every axis)."""
+    p = I.orszag_tang_3d(16, limiter=I.WENOZ).replace(stepper=I.RK3)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    o = oracle.Oracle(p, U0)
+    o.run(4)
+    for f in range(8):
+        scale = max(np.abs(U0[f]).sum(), np.abs(o.U[f]).sum(), 1.0)
+        assert abs(o.U[f].sum() - U0[f].sum()) <= 1e-13 * scale
+    p1 = I.brio_wu(64).replace(glm=1, limiter=I.WENOZ)
+    U1 = I.brio_wu_ic(p1)
+    p3 = p1.replace(n=(64, 4, 4))
+    U3 = np.broadcast_to(U1, (9, 4, 4, 64)).copy()
+    o1, o3 = oracle.Oracle(p1, U1), oracle.Oracle(p3, U3)
+    for _ in range(3):
+        dt, ch = o1.compute_dt()
+        o1.step(dt, ch)
+        o3.step(dt, ch)
+    assert np.array_equal(np.broadcast_to(o1.U, (9, 4, 4, 64)), o3.U)
