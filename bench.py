@@ -40,6 +40,11 @@ STAGE_BYTES_PER_CELL = {1: 2 * NV * 8, 2: 3 * NV * 8}
 # stage, 3D PLM-MC + HLLD(F* path) + GLM, no redundant work:
 # cons2prim 19 + 3 x PLM-MC 81 + 3 x face solve 243 + update 81 (+ 19 for the RK2 average in stage 2)
 FLOPS_CELL_STAGE = {1: 19 + 3 * 81 + 3 * 243 + 81, 2: 19 + 3 * 81 + 3 * 243 + 81 + 19}
+# WENO-Z: 71 ops per field and side -> 1278 per cell-direction; RK3 weights 27 per stage
+_WZ = 19 + 3 * 1278 + 3 * 243 + 81
+FLOPS_PER_LAUNCH_AVG = {"plm-rk2": (FLOPS_CELL_STAGE[1] + FLOPS_CELL_STAGE[2]) / 2.0,
+                        "wenoz-rk3": (_WZ + (_WZ + 27) + (_WZ + 28)) / 3.0}
+BYTES_PER_LAUNCH_AVG = {"plm-rk2": (2 * NV * 8 + 3 * NV * 8) / 2.0, "wenoz-rk3": (2 * NV * 8 + 3 * NV * 8 * 2) / 3.0}
 N_SM, FP64_LANES_PER_SM = 148, 64
 
 
@@ -108,16 +113,20 @@ WORKLOADS = {
 }
 
 
-def build_problem(workload: str, n_gpus: int, n: int):
+def build_problem(workload: str, n_gpus: int, n: int, scheme: str = "plm-rk2"):
     """per-GPU n^3 cube; with N GPUs the box is n x n x (n N) with z extent N (weak scaling)"""
     from paper_2510_24175_b200 import inputs as I
     if workload == "ot3d":
-        return I.orszag_tang_3d(n, nz=n * n_gpus, z_extent=float(n_gpus))
-    if workload == "blast3d":
-        return I.blast_3d(n, cubes=n_gpus)
-    if workload == "cpa3d":
-        return I.cpa_3d(n).replace(n=(n, n, n * n_gpus), hi=(1.0, 1.0, float(n_gpus)))
-    raise ValueError(workload)
+        p = I.orszag_tang_3d(n, nz=n * n_gpus, z_extent=float(n_gpus))
+    elif workload == "blast3d":
+        p = I.blast_3d(n, cubes=n_gpus)
+    elif workload == "cpa3d":
+        p = I.cpa_3d(n).replace(n=(n, n, n * n_gpus), hi=(1.0, 1.0, float(n_gpus)))
+    else:
+        raise ValueError(workload)
+    if scheme == "wenoz-rk3":
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    return p
 
 
 def build_ic(workload: str, p, z0: int, z1: int, chunk: int = 64):
@@ -141,11 +150,11 @@ def cpu_info():
         return "unknown"
 
 
-def oracle_sample(workload: str, n: int, nz_s: int, steps: int, warmup: int):
+def oracle_sample(workload: str, n: int, nz_s: int, steps: int, warmup: int, scheme: str = "plm-rk2"):
     """The CPU oracle, as it stands, on a bounded sample of the workload: the first nz_s planes of
     the n^3 initial condition as a periodic n x n x nz_s slab (same per-cell work)."""
     import oracle
-    full = build_problem(workload, 1, n)
+    full = build_problem(workload, 1, n, scheme)
     dz = (full.hi[2] - full.lo[2]) / full.n[2]
     p = full.replace(n=(n, n, nz_s), hi=(full.hi[0], full.hi[1], full.lo[2] + nz_s * dz))
     U = build_ic(workload, full, 0, nz_s)
@@ -166,7 +175,7 @@ def run_reference(args, rank, world):
         return
     n = args.n
     nz_s = max(4, min(n, (256 ** 3 // 4) // (n * n)))  # ~4.2 M cells per step
-    v, el, cores, p = oracle_sample(args.workload, n, nz_s, args.steps, args.warmup)
+    v, el, cores, p = oracle_sample(args.workload, n, nz_s, args.steps, args.warmup, args.scheme)
     sample = (f"CPU oracle (oracle/mhd_oracle.c, gcc -O2 -ffp-contract=off, OpenMP {cores} threads), "
               f"{args.steps} timed steps after {args.warmup} warm-up of a {n}x{n}x{nz_s} periodic slab of the "
               f"{n}^3 {args.workload} IC ({nz_s}/{n} of the workload's planes per step)")
@@ -189,6 +198,9 @@ def main():
     ap.add_argument("--impl", default="mhd", choices=["mhd", "reference"])
     ap.add_argument("--n", type=int, default=256, help="cells per axis per GPU (configs[2]: 256)")
     ap.add_argument("--workload", default="ot3d", choices=sorted(WORKLOADS))
+    ap.add_argument("--scheme", default="plm-rk2", choices=["plm-rk2", "wenoz-rk3"],
+                    help="plm-rk2: the north star's PLM-MC + HLLD + GLM + SSP-RK2 (default); wenoz-rk3: the "
+                         "paper's WENOZ + HLLD + GLM + SSP-RK3 (PAPER.md:179, 270)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=256, help="cpu_baseline sample: planes of the grid")
@@ -211,7 +223,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    p = build_problem(args.workload, world, args.n)
+    p = build_problem(args.workload, world, args.n, args.scheme)
     nz_loc = p.n[2] // world
     nccl_id = None
     if world > 1:
@@ -268,8 +280,8 @@ def main():
     dt_ms, dt_n = prof["dt"]
     cells_loc = p.cells // world
     stage_avg_s = stage_ms * 1e-3 / max(stage_n, 1)
-    flops_launch = cells_loc * (FLOPS_CELL_STAGE[1] + FLOPS_CELL_STAGE[2]) / 2.0  # stages alternate
-    bytes_launch = cells_loc * (STAGE_BYTES_PER_CELL[1] + STAGE_BYTES_PER_CELL[2]) / 2.0
+    flops_launch = cells_loc * FLOPS_PER_LAUNCH_AVG[args.scheme]  # average over the step's stages
+    bytes_launch = cells_loc * BYTES_PER_LAUNCH_AVG[args.scheme]
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     fp64_peak = N_SM * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12  # TFLOP/s, 1 op per lane per clock (no FMA)
     achieved = flops_launch / stage_avg_s / 1e12
@@ -283,13 +295,15 @@ def main():
             "traffic": ncu.get("dram_bytes_per_launch"),
             "kernel": "k_stage (fused cons2prim + PLM + GLM + HLL/HLLD + flux divergence + RK2 update)",
             "peak_kind": f"derived: {N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x {sm_mhz:.0f} MHz (recipe has no FMA)",
-            "flops_per_cell_stage": FLOPS_CELL_STAGE, "algorithmic_flops_per_launch": flops_launch,
+            "flops_per_cell_stage_avg": FLOPS_PER_LAUNCH_AVG[args.scheme], "algorithmic_flops_per_launch": flops_launch,
             "stage_ms_per_launch": stage_avg_s * 1e3, "stage_launches": stage_n,
             "stage_share_of_step": stage_ms / max(ms, 1e-9), "dt_ms_per_launch": dt_ms / max(dt_n, 1),
             "hbm": {"achieved": bytes_launch / stage_avg_s / 1e9, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                     "frac": bytes_launch / stage_avg_s / 1e9 / pk.get("hbm_gbs", 6537.3), "peak_kind": pk_kind,
                     "algorithmic_bytes_per_launch": bytes_launch},
-            "ncu": ncu or None}
+            "ncu": (ncu or None) if args.scheme == "plm-rk2" else None}
+    if args.scheme != "plm-rk2":
+        roof["traffic"] = None
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -317,7 +331,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         nz_s = min(args.cpu_planes, args.n, max(4, (256 ** 3) // (args.n * args.n)))
-        v, el, cores, pp = oracle_sample(args.workload, args.n, nz_s, 1, 0)
+        v, el, cores, pp = oracle_sample(args.workload, args.n, nz_s, 1, 0, args.scheme)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_info(),
                "sample": f"1 step (compute_dt + RK2 step) of a {args.n}x{args.n}x{nz_s} periodic slab of the "
                          f"{args.n}^3 {args.workload} IC, {el:.1f} s on {cores} OpenMP threads"}
@@ -328,7 +342,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{args.workload}_{args.n}^3_per_gpu ({WORKLOADS[args.workload]}; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
-                           "scheme": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4", "cells": cells,
+                           "scheme": {"plm-rk2": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4",
+                                      "wenoz-rk3": "WENOZ + HLLD + GLM, SSP-RK3, CFL 0.4"}[args.scheme], "cells": cells,
                            "parallelism": f"z-slab x{world}", "l2": "inputs larger than L2 (2 x 1.27 GB arrays per GPU)"},
                 "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * 3,
                 "e2e": e2e, "cpu_baseline": cpu, "diag": diag,

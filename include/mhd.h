@@ -48,7 +48,7 @@ enum {
   MHD_E_UNPHYSICAL = 6  /* rho <= 0 or non-finite state (see mhd_diag.first_bad_cell) */
 };
 enum { MHD_BC_PERIODIC = 0, MHD_BC_OUTFLOW = 1 };
-enum { MHD_LIM_MINMOD = 0, MHD_LIM_MC = 1 };
+enum { MHD_LIM_MINMOD = 0, MHD_LIM_MC = 1, MHD_LIM_WENOZ = 2 };  /* WENOZ: ghost width 3 (R31) */
 enum { MHD_RS_HLL = 0, MHD_RS_HLLD = 1 };
 enum { MHD_RK2 = 0, MHD_RK3 = 1 };
 
@@ -78,7 +78,7 @@ typedef struct {
 } mhd_scheme;
 
 /* Multi-GPU: z-slab decomposition over nranks GPUs.  NULL => 1 GPU, the
- * current CUDA device.  nranks must divide n[2] with n[2]/nranks >= 2.  nccl_id comes from
+ * current CUDA device.  nranks must divide n[2] with n[2]/nranks >= the ghost width.  nccl_id comes from
  * mhd_nccl_get_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
  * transport MHD_TRANSPORT_NCCL: one process per GPU, halos by ncclSend/ncclRecv overlapped
  * with the interior of each stage, dt by ncclAllReduce(max).
@@ -155,9 +155,10 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 
 /* Halo plan of a z slab (pure host logic, no GPU): the 4 transfers of one RK stage in posting
  * order, each as (peer rank or -1, 0 = send / 1 = recv, first storage plane, plane count);
- * storage planes are 0..nz_loc+3 with the 2 ghost planes at each end.  Returns MHD_E_ARG on
- * inconsistent arguments. */
-int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t plan[4][4]);
+ * storage planes are 0..nz_loc+2*ghost-1 with `ghost` ghost planes at each end (2 for PLM,
+ * 3 for WENOZ).  Returns MHD_E_ARG on inconsistent arguments. */
+int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
+                  int32_t plan[4][4]);
 
 /* Counters and the unphysical-state record (synchronising; collective when nranks > 1
  * only through mhd_compute_dt, which refreshes the global sums). */

@@ -158,18 +158,20 @@ StagePlan stage_plan(const mhd_ctx* c, int stage) {
   return p;
 }
 
-// a1 (z part).  Halo plan of one stage for a z slab: the transfers in posting order as
-// (peer, 0 send / 1 recv, first storage plane, planes).  Storage planes: 0,1 bottom ghosts,
-// 2..nz+1 interior, nz+2, nz+3 top ghosts.  Sends: top 2 interior planes -> up, bottom 2
-// interior planes -> down; receives: bottom ghosts <- down, top ghosts <- up.  The fixed
+// a1 (z part).  Halo plan of one stage for a z slab with g ghost planes per side (PLM 2,
+// WENO-Z 3): the transfers in posting order as (peer, 0 send / 1 recv, first storage plane,
+// planes).  Storage planes: 0..g-1 bottom ghosts, g..nz+g-1 interior, nz+g..nz+2g-1 top
+// ghosts.  Sends: top g interior planes -> up, bottom g interior planes -> down; receives:
+// bottom ghosts <- down, top ghosts <- up.  The fixed
 // posting order (send up, recv down, send down, recv up) pairs correctly with nranks = 2,
 // where both neighbours are the same peer (NCCL matches per peer in posting order).
-int halo_plan(int rank, int nranks, long long nz_glob, int z_periodic, int plan[4][4]) {
-  if (nranks < 1 || rank < 0 || rank >= nranks || nz_glob % nranks != 0 || nz_glob / nranks < 2) return MHD_E_ARG;
+int halo_plan(int rank, int nranks, long long nz_glob, int z_periodic, int g, int plan[4][4]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || g < 1 || nz_glob % nranks != 0 || nz_glob / nranks < g)
+    return MHD_E_ARG;
   const int nz = (int)(nz_glob / nranks);
   const int up = (nranks > 1 && (z_periodic || rank < nranks - 1)) ? (rank + 1) % nranks : -1;
   const int down = (nranks > 1 && (z_periodic || rank > 0)) ? (rank + nranks - 1) % nranks : -1;
-  const int rows[4][4] = {{up, 0, nz, 2}, {down, 1, 0, 2}, {down, 0, 2, 2}, {up, 1, nz + 2, 2}};
+  const int rows[4][4] = {{up, 0, nz, g}, {down, 1, 0, g}, {down, 0, g, g}, {up, 1, nz + g, g}};
   for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 4; ++j) plan[i][j] = rows[i][j];
   return MHD_OK;
@@ -183,17 +185,15 @@ int fill_z_ghosts_local(mhd_ctx* c, double* U) {
   const int nz = c->nzl, g = c->gz;
   auto P = [&](int zs) { return U + (size_t)zs * pe; };
   const bool peri = c->bc_lo[2] == MHD_BC_PERIODIC;
-  if (c->nranks == 1 && peri) {
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), 2 * pb, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->nranks == 1 && peri) {  // U[-m] = U[N-m], U[N-1+m] = U[m-1]: two contiguous g-plane blocks
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), g * pb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), g * pb, cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (!peri && c->rank == 0) {  // outflow: U[-2] = U[-1] = U[0]
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(1), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
-  }
-  if (!peri && c->rank == c->nranks - 1) {  // outflow: U[N] = U[N+1] = U[N-1]
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g + 1), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
+  for (int m = 0; m < g; ++m) {
+    if (!peri && c->rank == 0)  // outflow: U[-m] = U[0]
+      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(m), P(g), pb, cudaMemcpyDeviceToDevice, c->stream));
+    if (!peri && c->rank == c->nranks - 1)  // outflow: U[N-1+m] = U[N-1]
+      CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g + m), P(nz + g - 1), pb, cudaMemcpyDeviceToDevice, c->stream));
   }
   return MHD_OK;
 }
@@ -203,7 +203,7 @@ int fill_z_ghosts_local(mhd_ctx* c, double* U) {
 int exchange_nccl(mhd_ctx* c, double* U) {
   const size_t pe = plane_elems(c);
   int plan[4][4];
-  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, plan))
+  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, c->gz, plan))
     return set_err(c, MHD_E_ARG, "halo plan");
   CUDA_OR_RETURN(c, cudaEventRecord(c->ev_ready, c->stream));
   CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
@@ -226,19 +226,20 @@ int exchange_nccl(mhd_ctx* c, double* U) {
 // array (the same array role: U^n or U*)
 int exchange_local(mhd_ctx* c, int stage) {
   const size_t pe = plane_elems(c), pb = pe * sizeof(double);
+  const int g = c->gz;
   int plan[4][4];
-  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, plan))
+  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, g, plan))
     return set_err(c, MHD_E_ARG, "halo plan");
   double* mine = stage_plan(c, stage).in;
   for (int i = 0; i < 4; ++i) {
     if (plan[i][0] < 0 || plan[i][1] != 1) continue;  // receives only
     const mhd_ctx* peer = c->group[plan[i][0]];
     const double* theirs = stage_plan(peer, stage).in;
-    // the peer sends its top interior planes to its up neighbour, bottom ones to its down
-    // neighbour: my bottom ghosts (recv from down) <- down's storage planes nz, nz+1;
-    // my top ghosts (recv from up) <- up's storage planes 2, 3
-    const int src = (plan[i][2] == 0) ? peer->nzl : 2;
-    CUDA_OR_RETURN(c, cudaMemcpyAsync(mine + (size_t)plan[i][2] * pe, theirs + (size_t)src * pe, 2 * pb,
+    // the peer sends its top g interior planes to its up neighbour, its bottom g to its down
+    // neighbour: my bottom ghosts (recv from down) <- down's storage planes nz..nz+g-1; my top
+    // ghosts (recv from up) <- up's storage planes g..2g-1
+    const int src = (plan[i][2] == 0) ? peer->nzl : g;
+    CUDA_OR_RETURN(c, cudaMemcpyAsync(mine + (size_t)plan[i][2] * pe, theirs + (size_t)src * pe, g * pb,
                                       cudaMemcpyDeviceToDevice, c->stream));
   }
   return MHD_OK;
@@ -427,7 +428,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     c->scheme.glm_alpha = 0.1;
     c->scheme.p_floor = 1e-12;
   }
-  if ((c->scheme.limiter != MHD_LIM_MINMOD && c->scheme.limiter != MHD_LIM_MC) ||
+  if ((c->scheme.limiter != MHD_LIM_MINMOD && c->scheme.limiter != MHD_LIM_MC && c->scheme.limiter != MHD_LIM_WENOZ) ||
       (c->scheme.riemann != MHD_RS_HLL && c->scheme.riemann != MHD_RS_HLLD) || (c->scheme.glm != 0 && c->scheme.glm != 1) ||
       (c->scheme.stepper != MHD_RK2 && c->scheme.stepper != MHD_RK3) ||
       !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm)) {
@@ -460,7 +461,11 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->ny = (int)c->n[1];
   c->nzl = (int)(c->n[2] / c->nranks);
   c->zoff = (long long)c->nzl * c->rank;
-  c->gz = c->dim == 3 ? 2 : 0;
+  c->gz = c->dim == 3 ? (c->scheme.limiter == MHD_LIM_WENOZ ? 3 : 2) : 0;
+  if (c->dim == 3 && c->nzl < c->gz) {
+    delete c;
+    return MHD_E_ARG;
+  }
   const bool zper = c->bc_lo[2] == MHD_BC_PERIODIC;
   c->up = (c->nranks > 1 && (zper || c->rank < c->nranks - 1)) ? (c->rank + 1) % c->nranks : -1;
   c->down = (c->nranks > 1 && (zper || c->rank > 0)) ? (c->rank + c->nranks - 1) % c->nranks : -1;
@@ -471,7 +476,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   {
     const int ty = mhd::stage_tile_rows(c->dim);
     const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + ty - 1) / ty);
-    const long long slots = (long long)c->nsm * mhd::stage_ctas_per_sm(c->dim, c->nv, c->scheme.riemann);
+    const long long slots = (long long)c->nsm * mhd::stage_ctas_per_sm(c->dim, c->nv, c->scheme.riemann, c->scheme.limiter);
     long long best_kz = c->nzl;
     double best = 1e300;
     for (long long chunks = 1; chunks <= c->nzl; ++chunks) {
@@ -650,10 +655,11 @@ int mhd_step(mhd_ctx* c, double dt) {
     double* U = stage_plan(c, stage).in;
     if ((rc = fill_z_ghosts_local(c, U))) return rc;
     if (c->nranks > 1 && c->dim == 3) {
-      // halo exchange on the comm stream, overlapped with the interior planes [2, nz-2)
-      // (their stencil never reads a ghost plane); then the 2 + 2 boundary planes
+      // halo exchange on the comm stream, overlapped with the interior planes [g, nz-g)
+      // (their stencil never reads a ghost plane); then the g + g boundary planes
       if ((rc = exchange_nccl(c, U))) return rc;
-      const int lo = 2 < c->nzl ? 2 : c->nzl, hi = c->nzl - 2 > lo ? c->nzl - 2 : lo;
+      const int g = c->gz;
+      const int lo = g < c->nzl ? g : c->nzl, hi = c->nzl - g > lo ? c->nzl - g : lo;
       if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
       CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
       if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
@@ -667,9 +673,10 @@ int mhd_step(mhd_ctx* c, double dt) {
   return MHD_OK;
 }
 
-int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t plan[4][4]) {
+int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
+                  int32_t plan[4][4]) {
   if (!plan) return MHD_E_ARG;
-  return halo_plan(rank, nranks, nz_glob, z_periodic, plan);
+  return halo_plan(rank, nranks, nz_glob, z_periodic, ghost, plan);
 }
 
 namespace {

@@ -86,11 +86,11 @@ __device__ __forceinline__ void flush_counters(int nthreads, unsigned long long*
 #define MHD_OCC3 2
 #endif
 // ---------------------------------------------------------------------------------------
-template <int DIM, int NV, int TY>
+template <int DIM, int NV, int TY, int G>
 struct StageSmem {
   static constexpr int TX = 32;
-  static constexpr int HY = DIM >= 2 ? 2 : 0;
-  static constexpr int PW = TX + 4;
+  static constexpr int HY = DIM >= 2 ? G : 0;  // y halo rows (G = stencil half-width: PLM 2, WENOZ 3)
+  static constexpr int PW = TX + 2 * G;
   static constexpr int PH = TY + 2 * HY;
   static constexpr int NT = 32 * (TY + 1);  // TY cell warps + 1 edge warp
   static constexpr int nVc = NV * PH * PW;
@@ -117,9 +117,10 @@ struct StageOcc {
 // so every warp runs at most 3 face solves per plane and the per-plane barriers do not wait
 // on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
-template <int DIM, int NV, int RS, int TY>
+template <int DIM, int NV, int RS, int TY, int WZ>
 __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_stage(StageArgs a) {
-  using S = StageSmem<DIM, NV, TY>;
+  constexpr int G = WZ ? 3 : 2;  // reconstruction half-width: PLM 2, WENO-Z 3
+  using S = StageSmem<DIM, NV, TY, G>;
   constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH, NT = S::NT;
   constexpr int NC = 32 * TY;        // threads of the cell warps
   extern __shared__ double smem[];
@@ -180,22 +181,22 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
     if (cellw) {
       double v[NV];
       convert_own(k, v, count_own);
-      store_vc(ty + HY, tx + 2, v);
+      store_vc(ty + HY, tx + G, v);
     }
-    constexpr int NXH = 4 * TY;
-    constexpr int NYH = (DIM >= 2) ? 4 * TX : 0;
+    constexpr int NXH = 2 * G * TY;
+    constexpr int NYH = (DIM >= 2) ? 2 * G * TX : 0;
     for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {  // the edge warp takes the first slots
       double v[NV];
       if (h < NXH) {
-        const int r = h >> 2, w = h & 3;
-        const int col = (w < 2) ? w : TX + w;  // padded cols 0,1 | TX+2, TX+3
-        convert_any(k, x0 + col - 2, y0 + r, v);
+        const int r = h / (2 * G), w = h % (2 * G);
+        const int col = (w < G) ? w : TX + w;  // padded cols 0..G-1 | TX+G..TX+2G-1
+        convert_any(k, x0 + col - G, y0 + r, v);
         store_vc(r + HY, col, v);
       } else {
         const int j = h - NXH, rs = j / TX, col = j % TX;
-        const int r = (rs < 2) ? rs : TY + rs;  // padded rows 0,1 | TY+2, TY+3
+        const int r = (rs < G) ? rs : TY + rs;  // padded rows 0..G-1 | TY+G..TY+2G-1
         convert_any(k, x0 + col, y0 + r - HY, v);
-        store_vc(r, col + 2, v);
+        store_vc(r, col + G, v);
       }
     }
   };
@@ -205,16 +206,27 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
   if constexpr (DIM == 3) {
     // V+(kb-1) into Vpz; V(kb-1) as the centre of Vc (read by the z job of iteration kb-1)
     if (cellw) {
-      double qA[NV], qB[NV], qC[NV], qp[NV], qm[NV];
-      convert_own(kb - 2, qA, false);
-      convert_own(kb - 1, qB, false);
-      convert_own(kb, qC, true);  // the counted conversion of plane kb
-      plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
+      double qp[NV], qm[NV], qB[NV];
+      if constexpr (WZ) {  // V+(kb-1) from V(kb-3..kb+1)
+        double qAA[NV], qA[NV], qC[NV], qCC[NV];
+        convert_own(kb - 3, qAA, false);
+        convert_own(kb - 2, qA, false);
+        convert_own(kb - 1, qB, false);
+        convert_own(kb, qC, true);  // the counted conversions of planes kb, kb+1
+        convert_own(kb + 1, qCC, kb + 1 < ke);
+        weno_cell<NV>(qAA, qA, qB, qC, qCC, qp, qm);
+      } else {  // V+(kb-1) from V(kb-2..kb)
+        double qA[NV], qC[NV];
+        convert_own(kb - 2, qA, false);
+        convert_own(kb - 1, qB, false);
+        convert_own(kb, qC, true);  // the counted conversion of plane kb
+        plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
+      }
       double wp[NV];
       to_normal<NV, 2>(qp, wp);  // Vpz is kept in the z normal frame
 #pragma unroll
       for (int f = 0; f < NV; ++f) Vpz[f * NC + tid] = wp[f];
-      store_vc(ty + HY, tx + 2, qB);
+      store_vc(ty + HY, tx + G, qB);
     }
     kstart = kb - 1;
     __syncthreads();
@@ -231,8 +243,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
       // cell of planes k+1, k+2 (the z job) and of plane k (update; U^n in stage 2) into L1
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
-        prefetch_l2(a.Uin + plane_off(k + 3 < nzl + a.gz ? k + 3 : k) + f * fstride + own_cell);
-        prefetch_l1(a.Uin + plane_off(k + 2) + f * fstride + own_cell);
+        prefetch_l2(a.Uin + plane_off(k + G + 1 < nzl + a.gz ? k + G + 1 : k) + f * fstride + own_cell);
+        prefetch_l1(a.Uin + plane_off(k + G) + f * fstride + own_cell);
         if (full && a.mode != 0) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
       }
     }
@@ -286,12 +298,20 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
           double q0[NV], q1[NV], q2[NV], qp[NV], qm[NV];
 #pragma unroll
           for (int f = 0; f < NV; ++f) {
-            q0[f] = Vc[(f * PH + ty + HY) * PW + tx + 2];
+            q0[f] = Vc[(f * PH + ty + HY) * PW + tx + G];
             wl[f] = Vpz[f * NC + tid];
           }
           convert_own(k + 1, q1, false);
-          convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
-          fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);  // cell k+1
+          if constexpr (WZ) {  // cell k+1 from V(k-1..k+3); plane k+3 is first touched here
+            double qm1[NV], q3[NV];
+            convert_own(k - 1, qm1, false);
+            convert_own(k + 2, q2, false);
+            convert_own(k + 3, q3, k + 3 >= kb && k + 3 < ke);
+            fb = weno_cell<NV>(qm1, q0, q1, q2, q3, qp, qm);
+          } else {  // cell k+1 from V(k..k+2); plane k+2 is first touched here
+            convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
+            fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);
+          }
           double wp[NV];
           to_normal<NV, 2>(qp, wp);
           to_normal<NV, 2>(qm, wr);
@@ -300,16 +320,32 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
         } else {
           const int s = (d == 0) ? 1 : PW;
           double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
+          if constexpr (WZ) {  // left cell from v[-3..1], right cell from v[-2..2]
+            double qaa[NV], qdd[NV];
 #pragma unroll
-          for (int n = 0; n < NV; ++n) {
-            const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + 2;
-            qa[n] = base[-2 * s];
-            qb[n] = base[-s];
-            qc[n] = base[0];
-            qd[n] = base[s];
+            for (int n = 0; n < NV; ++n) {
+              const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
+              qaa[n] = base[-3 * s];
+              qa[n] = base[-2 * s];
+              qb[n] = base[-s];
+              qc[n] = base[0];
+              qd[n] = base[s];
+              qdd[n] = base[2 * s];
+            }
+            weno_cell<NV>(qaa, qa, qb, qc, qd, wl, tmp);       // left cell: V+
+            fb = weno_cell<NV>(qa, qb, qc, qd, qdd, tmp, wr);  // right cell: V-
+          } else {
+#pragma unroll
+            for (int n = 0; n < NV; ++n) {
+              const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
+              qa[n] = base[-2 * s];
+              qb[n] = base[-s];
+              qc[n] = base[0];
+              qd[n] = base[s];
+            }
+            plm_cell<NV>(c.limiter, qa, qb, qc, wl, tmp);       // left cell: V+
+            fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, wr);  // right cell: V-
           }
-          plm_cell<NV>(c.limiter, qa, qb, qc, wl, tmp);       // left cell: V+
-          fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, wr);  // right cell: V-
         }
         cnt_fb += (fb && cnt_right) ? 1 : 0;
       }
@@ -500,10 +536,10 @@ __global__ void k_face_flux(const double* __restrict__ VL, const double* __restr
 // ---------------------------------------------------------------------------------------
 // host-side launchers (explicit instantiations)
 // ---------------------------------------------------------------------------------------
-template <int DIM, int NV, int RS, int TY>
+template <int DIM, int NV, int RS, int TY, int WZ>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
-  using S = StageSmem<DIM, NV, TY>;
-  auto kern = k_stage<DIM, NV, RS, TY>;
+  using S = StageSmem<DIM, NV, TY, WZ ? 3 : 2>;
+  auto kern = k_stage<DIM, NV, RS, TY, WZ>;
   static bool attr_set = false;
   static size_t extra = 0;  // MHD_EXTRA_SMEM (bytes): measurement knob for the L1 carve-out
   if (!attr_set) {
@@ -525,38 +561,50 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
 #ifndef MHD_TY2
 #define MHD_TY2 5
 #endif
-cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
+template <int WZ>
+static cudaError_t launch_stage_w(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
   if (dim == 3) {
-    if (riemann) return launch_stage_t<3, 9, 1, MHD_TY3>(a, st);
-    return launch_stage_t<3, 9, 0, MHD_TY3>(a, st);
+    if (riemann) return launch_stage_t<3, 9, 1, MHD_TY3, WZ>(a, st);
+    return launch_stage_t<3, 9, 0, MHD_TY3, WZ>(a, st);
   }
   if (dim == 2) {
-    if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2>(a, st);
-    return launch_stage_t<2, 9, 0, MHD_TY2>(a, st);
+    if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2, WZ>(a, st);
+    return launch_stage_t<2, 9, 0, MHD_TY2, WZ>(a, st);
   }
   if (nv == 9) {
-    if (riemann) return launch_stage_t<1, 9, 1, 1>(a, st);
-    return launch_stage_t<1, 9, 0, 1>(a, st);
+    if (riemann) return launch_stage_t<1, 9, 1, 1, WZ>(a, st);
+    return launch_stage_t<1, 9, 0, 1, WZ>(a, st);
   }
-  if (riemann) return launch_stage_t<1, 8, 1, 1>(a, st);
-  return launch_stage_t<1, 8, 0, 1>(a, st);
+  if (riemann) return launch_stage_t<1, 8, 1, 1, WZ>(a, st);
+  return launch_stage_t<1, 8, 0, 1, WZ>(a, st);
+}
+
+cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
+  // limiter 2 = WENO-Z (ghost width 3); 0/1 = PLM minmod/MC (runtime branch inside the kernel)
+  if (a.c.limiter == 2) return launch_stage_w<1>(dim, nv, riemann, a, st);
+  return launch_stage_w<0>(dim, nv, riemann, a, st);
 }
 
 int stage_tile_rows(int dim) { return dim == 3 ? MHD_TY3 : (dim == 2 ? MHD_TY2 : 1); }
 
-template <int DIM, int NV, int RS, int TY>
+template <int DIM, int NV, int RS, int TY, int WZ>
 static int ctas_per_sm_t() {
-  using S = StageSmem<DIM, NV, TY>;
-  auto kern = k_stage<DIM, NV, RS, TY>;
+  using S = StageSmem<DIM, NV, TY, WZ ? 3 : 2>;
+  auto kern = k_stage<DIM, NV, RS, TY, WZ>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, S::NT, S::bytes) != cudaSuccess) n = 1;
   return n > 0 ? n : 1;
 }
 
-int stage_ctas_per_sm(int dim, int nv, int riemann) {
-  if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3>() : ctas_per_sm_t<3, 9, 0, MHD_TY3>();
-  if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2>() : ctas_per_sm_t<2, 9, 0, MHD_TY2>();
+int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter) {
+  if (limiter == 2) {
+    if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3, 1>() : ctas_per_sm_t<3, 9, 0, MHD_TY3, 1>();
+    if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 1>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 1>();
+    return 1;
+  }
+  if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3, 0>() : ctas_per_sm_t<3, 9, 0, MHD_TY3, 0>();
+  if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 0>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 0>();
   return 1;
 }
 

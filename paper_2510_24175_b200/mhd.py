@@ -98,7 +98,7 @@ def load() -> C.CDLL:
     L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.mhd_group_compute_dt.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(C.c_double)]
     L.mhd_group_step.argtypes = [C.POINTER(P), C.c_int32, C.c_double]
-    L.mhd_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]
+    L.mhd_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
     _lib = L
     return L
 
@@ -115,11 +115,11 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def halo_plan(rank: int, nranks: int, nz_glob: int, z_periodic: bool = True):
+def halo_plan(rank: int, nranks: int, nz_glob: int, z_periodic: bool = True, ghost: int = 2):
     """The 4 transfers of one RK stage for a z slab: rows (peer, 0 send / 1 recv, first storage
     plane, planes) in posting order (pure host logic of libmhd, usable without a GPU)."""
     buf = (C.c_int32 * 16)()
-    rc = load().mhd_halo_plan(rank, nranks, nz_glob, 1 if z_periodic else 0, buf)
+    rc = load().mhd_halo_plan(rank, nranks, nz_glob, 1 if z_periodic else 0, ghost, buf)
     if rc:
         raise MhdError(rc, "mhd_halo_plan")
     return [tuple(buf[4 * i:4 * i + 4]) for i in range(4)]

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, nz_glob, periodic, q):
+def _worker(rank, world, port, nz_glob, periodic, ghost, q):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -34,9 +34,10 @@ def _worker(rank, world, port, nz_glob, periodic, q):
         G = rng.standard_normal((nz_glob, nv, ny, nx))  # global interior, storage order [z][f][y][x]
         nz = nz_glob // world
         z0 = rank * nz
-        S = np.full((nz + 4, nv, ny, nx), np.nan)
-        S[2:nz + 2] = G[z0:z0 + nz]
-        plan = mhd.halo_plan(rank, world, nz_glob, periodic)
+        g = ghost
+        S = np.full((nz + 2 * g, nv, ny, nx), np.nan)
+        S[g:nz + g] = G[z0:z0 + nz]
+        plan = mhd.halo_plan(rank, world, nz_glob, periodic, ghost)
         reqs = []
         for peer, kind, first, count in plan:  # posting order of the plan
             if peer < 0:
@@ -52,12 +53,13 @@ def _worker(rank, world, port, nz_glob, periodic, q):
             else:
                 r.wait()
         ok = True
-        for g, zglob in ((0, z0 - 2), (1, z0 - 1), (nz + 2, z0 + nz), (nz + 3, z0 + nz + 1)):
+        pairs = [(m, z0 - g + m) for m in range(g)] + [(nz + g + m, z0 + nz + m) for m in range(g)]
+        for sp, zglob in pairs:
             if 0 <= zglob < nz_glob or periodic:
-                if not np.array_equal(S[g], G[zglob % nz_glob]):
+                if not np.array_equal(S[sp], G[zglob % nz_glob]):
                     ok = False
             else:
-                ok = ok and np.isnan(S[g]).all()  # domain edge: filled locally (outflow copy)
+                ok = ok and np.isnan(S[sp]).all()  # domain edge: filled locally (outflow copy)
         ids = [mhd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(ids, src=0)
         q.put((rank, ok, ids[0]))
@@ -65,14 +67,14 @@ def _worker(rank, world, port, nz_glob, periodic, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("periodic", [True, False])
-def test_two_rank_halo_plan_with_gloo(periodic):
+@pytest.mark.parametrize("periodic,ghost", [(True, 2), (False, 2), (True, 3)])
+def test_two_rank_halo_plan_with_gloo(periodic, ghost):
     from paper_2510_24175_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, 12, periodic, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 12, periodic, ghost, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
@@ -94,3 +96,6 @@ def test_halo_plan_shapes():
     assert mhd.halo_plan(1, 4, 64)[0] == (2, 0, 16, 2) and mhd.halo_plan(1, 4, 64)[3] == (2, 1, 18, 2)
     with pytest.raises(mhd.MhdError):
         mhd.halo_plan(0, 3, 64)  # 3 does not divide 64
+    assert mhd.halo_plan(1, 4, 64, True, 3)[0] == (2, 0, 16, 3) and mhd.halo_plan(1, 4, 64, True, 3)[3] == (2, 1, 19, 3)
+    with pytest.raises(mhd.MhdError):
+        mhd.halo_plan(0, 32, 64, True, 3)  # slab of 2 planes < ghost width 3

@@ -344,3 +344,55 @@ def test_rk3_slab_group_bitwise(mhd):
     U4 = g.get_state()
     g.destroy()
     assert np.array_equal(log1, log4) and np.array_equal(U1, U4)
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) row 3: WENO-Z reconstruction (ghost width 3), the paper's WENOZ + HLLD + RK3 + GLM
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["ot3d_rk3", "ot3d_rk2_hll", "brio_wu", "ot2d", "outflow_z"])
+def test_wenoz_parity(mhd, case):
+    if case.startswith("ot3d"):
+        p = I.orszag_tang_3d(32, limiter=I.WENOZ).replace(n=(40, 21, 19), hi=(1.25, 0.65625, 0.59375))
+        if case == "ot3d_rk3":
+            p = p.replace(stepper=I.RK3)
+        else:
+            p = p.replace(riemann=I.HLL)
+        U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+        res = run_both(mhd, p, U0, 8)
+    elif case == "brio_wu":
+        p = I.brio_wu(512).replace(limiter=I.WENOZ, stepper=I.RK3)
+        res = run_both(mhd, p, I.brio_wu_ic(p), 100000, p.t_end)
+    elif case == "ot2d":
+        p = I.orszag_tang_2d(64, limiter=I.WENOZ).replace(stepper=I.RK3)
+        res = run_both(mhd, p, I.orszag_tang_2d_ic(p), 60)
+    else:
+        n = 48
+        p = I.Problem("bwz", (8, 8, n), bc=(I.OUTFLOW,) * 3, gamma=2.0, glm=1, riemann=I.HLLD, limiter=I.WENOZ,
+                      stepper=I.RK3)
+        U1 = I.brio_wu_ic(I.brio_wu(n).replace(glm=1))[:, 0, 0, :]
+        U = np.zeros(p.shape)
+        for f in range(9):
+            src = f
+            if 1 <= f <= 3:
+                src = 1 + (f - 1 - 2) % 3
+            if 5 <= f <= 7:
+                src = 5 + (f - 5 - 2) % 3
+            U[f] = U1[src][:, None, None]
+        res = run_both(mhd, p, U, 30)
+    assert_parity(*res)
+
+
+def test_wenoz_slab_group_bitwise(mhd):
+    p = I.orszag_tang_3d(24, limiter=I.WENOZ).replace(stepper=I.RK3)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(4)
+    U1 = s.get_state()
+    s.destroy()
+    g = mhd.SolverGroup(p, 4)  # slabs of 6 planes >= ghost width 3
+    g.set_state(U0)
+    log4 = g.run(4)
+    U4 = g.get_state()
+    g.destroy()
+    assert np.array_equal(log1, log4) and np.array_equal(U1, U4)
