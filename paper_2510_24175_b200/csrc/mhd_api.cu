@@ -474,7 +474,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   // face and converts 2 extra planes).  Pick the chunk count minimising waves x chunk cost
   // (MHD_KZ overrides, for measurements).
   {
-    const int ty = mhd::stage_tile_rows(c->dim);
+    const int ty = mhd::stage_tile_rows(c->dim, c->scheme.limiter);
     const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + ty - 1) / ty);
     const long long slots = (long long)c->nsm * mhd::stage_ctas_per_sm(c->dim, c->nv, c->scheme.riemann, c->scheme.limiter);
     long long best_kz = c->nzl;

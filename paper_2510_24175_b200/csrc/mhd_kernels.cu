@@ -100,9 +100,12 @@ struct StageSmem {
   static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx);
 };
 
-template <int DIM, int TY>
+#ifndef MHD_OCCW
+#define MHD_OCCW 2
+#endif
+template <int DIM, int TY, int WZ>
 struct StageOcc {
-  static constexpr int value = DIM == 3 ? MHD_OCC3 : (DIM == 2 ? 2 : 4);
+  static constexpr int value = DIM == 3 ? (WZ ? MHD_OCCW : MHD_OCC3) : (DIM == 2 ? 2 : 4);
 };
 
 // One CTA: a 32 x TY cell tile (TY "cell warps", lane = x) plus one "edge warp", marching
@@ -118,7 +121,7 @@ struct StageOcc {
 // on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
 template <int DIM, int NV, int RS, int TY, int WZ>
-__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_stage(StageArgs a) {
+__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value)) k_stage(StageArgs a) {
   constexpr int G = WZ ? 3 : 2;  // reconstruction half-width: PLM 2, WENO-Z 3
   using S = StageSmem<DIM, NV, TY, G>;
   constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH, NT = S::NT;
@@ -332,8 +335,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY>::value)) k_s
               qd[n] = base[s];
               qdd[n] = base[2 * s];
             }
-            weno_cell<NV>(qaa, qa, qb, qc, qd, wl, tmp);       // left cell: V+
-            fb = weno_cell<NV>(qa, qb, qc, qd, qdd, tmp, wr);  // right cell: V-
+            weno_side<NV, true>(qaa, qa, qb, qc, qd, wl);        // left cell: V+
+            fb = weno_side<NV, false>(qa, qb, qc, qd, qdd, wr);  // right cell: V-
           } else {
 #pragma unroll
             for (int n = 0; n < NV; ++n) {
@@ -561,11 +564,15 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
 #ifndef MHD_TY2
 #define MHD_TY2 5
 #endif
+#ifndef MHD_TYW3
+#define MHD_TYW3 5
+#endif
 template <int WZ>
 static cudaError_t launch_stage_w(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
   if (dim == 3) {
-    if (riemann) return launch_stage_t<3, 9, 1, MHD_TY3, WZ>(a, st);
-    return launch_stage_t<3, 9, 0, MHD_TY3, WZ>(a, st);
+    constexpr int TY3 = WZ ? MHD_TYW3 : MHD_TY3;
+    if (riemann) return launch_stage_t<3, 9, 1, TY3, WZ>(a, st);
+    return launch_stage_t<3, 9, 0, TY3, WZ>(a, st);
   }
   if (dim == 2) {
     if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2, WZ>(a, st);
@@ -585,7 +592,9 @@ cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaS
   return launch_stage_w<0>(dim, nv, riemann, a, st);
 }
 
-int stage_tile_rows(int dim) { return dim == 3 ? MHD_TY3 : (dim == 2 ? MHD_TY2 : 1); }
+int stage_tile_rows(int dim, int limiter) {
+  return dim == 3 ? (limiter == 2 ? MHD_TYW3 : MHD_TY3) : (dim == 2 ? MHD_TY2 : 1);
+}
 
 template <int DIM, int NV, int RS, int TY, int WZ>
 static int ctas_per_sm_t() {
@@ -599,7 +608,7 @@ static int ctas_per_sm_t() {
 
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter) {
   if (limiter == 2) {
-    if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3, 1>() : ctas_per_sm_t<3, 9, 0, MHD_TY3, 1>();
+    if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TYW3, 1>() : ctas_per_sm_t<3, 9, 0, MHD_TYW3, 1>();
     if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 1>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 1>();
     return 1;
   }

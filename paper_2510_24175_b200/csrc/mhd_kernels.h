@@ -41,7 +41,7 @@ struct DtArgs {
 };
 
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st);
-int stage_tile_rows(int dim);
+int stage_tile_rows(int dim, int limiter);
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter);  // resident CTAs per SM of the stage kernel
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st);
 cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, int nzl, int gz, int to_internal,
