@@ -51,35 +51,6 @@ __device__ __forceinline__ void load_cell(const double* __restrict__ U, size_t p
 __device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
-// block-wide sum of three per-thread counters, one atomicAdd per counter per block
-__device__ __forceinline__ void flush_counters(int nthreads, unsigned long long* gcnt, int c0, int c1, int c2) {
-  __shared__ int red[3][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c0 += __shfl_down_sync(0xffffffffu, c0, o);
-    c1 += __shfl_down_sync(0xffffffffu, c1, o);
-    c2 += __shfl_down_sync(0xffffffffu, c2, o);
-  }
-  if (lane == 0) {
-    red[0][w] = c0;
-    red[1][w] = c1;
-    red[2][w] = c2;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s0 = 0, s1 = 0, s2 = 0;
-    for (int i = 0; i < (nthreads + 31) / 32; ++i) {
-      s0 += red[0][i];
-      s1 += red[1][i];
-      s2 += red[2][i];
-    }
-    if (s0) atomicAdd(gcnt + 0, (unsigned long long)s0);
-    if (s1) atomicAdd(gcnt + 1, (unsigned long long)s1);
-    if (s2) atomicAdd(gcnt + 2, (unsigned long long)s2);
-  }
-}
-
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
 #ifndef MHD_OCC3
@@ -144,8 +115,15 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
   const size_t pstride = fstride * NV;
   const int kb = a.zb + blockIdx.z * a.kz;  // this CTA's z chunk inside [zb, ze)
   const int ke = min(kb + a.kz, a.ze);
-  int cnt_floor = 0, cnt_fb = 0, cnt_hll = 0;
-  unsigned long long badidx = ULLONG_MAX;
+  // rare events (floors, fallbacks, HLL fallbacks, bad cells) go to shared-memory counters by
+  // atomics only when they happen: no registers held for them across the face solves
+  __shared__ int s_cnt[3];
+  __shared__ unsigned long long s_bad;
+  if (tid == 0) {
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+    s_bad = ULLONG_MAX;
+  }
+  __syncthreads();
 
   // own-cell offset (x, y wrapped for ragged lanes: they compute a valid duplicate and never store)
   const int wx = wrap_index(gx, nx, a.bcx[0], a.bcx[1]);
@@ -163,8 +141,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
     load_cell<NV>(a.Uin, plane_off(k), fstride, own_cell, u);
     const bool fl = cons2prim<NV>(u, v, c.gm1, c.p_floor);
     if (count && own) {
-      cnt_floor += fl ? 1 : 0;
-      if (bad_state<NV>(u)) badidx = min(badidx, glin(k));
+      if (fl) atomicAdd(&s_cnt[0], 1);
+      if (bad_state<NV>(u)) atomicMin(&s_bad, glin(k));
     }
   };
   auto convert_any = [&](int k, int x, int y, double* v) {
@@ -350,12 +328,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
             fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, wr);  // right cell: V-
           }
         }
-        cnt_fb += (fb && cnt_right) ? 1 : 0;
+        if (fb && cnt_right) atomicAdd(&s_cnt[1], 1);
       }
       // ---- the face solve (single instance)
       double fn[NV];
       const int fell = face_flux<NV, RS>(wl, wr, c, fn);
-      cnt_hll += (fell && cnt_face) ? 1 : 0;
+      if (fell && cnt_face) atomicAdd(&s_cnt[2], 1);
       // ---- scatter (back to x,y,z components through the same field map)
       if (job == 0) {
         double fz[NV];
@@ -363,9 +341,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
         double* dst = Fz + ((k + 1) & 1) * S::nCol;
 #pragma unroll
         for (int f = 0; f < NV; ++f) dst[f * NC + tid] = fz[f];
-      } else if (d == 1) {
+      } else if (d == 1) {  // y frame (y, z, x): normal components n -> fields (0, 2, 3, 1, 4, 6, 7, 5, 8)
+        double fy[NV];
+        from_normal<NV, 1>(fn, fy);
 #pragma unroll
-        for (int n = 0; n < NV; ++n) Fy[(fo[n] * (TY + 1) + row) * TX + col] = fn[n];
+        for (int f = 0; f < NV; ++f) Fy[(f * (TY + 1) + row) * TX + col] = fy[f];
       } else {
 #pragma unroll
         for (int n = 0; n < NV; ++n) Fx[(n * TY + row) * (TX + 1) + col] = fn[n];
@@ -414,8 +394,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
       }
     }
   }
-  if (badidx != ULLONG_MAX) atomicMin(a.bad + a.stage, badidx);
-  flush_counters(NT, a.counters, cnt_floor, cnt_fb, cnt_hll);
+  __syncthreads();
+  if (tid == 0) {
+    if (s_bad != ULLONG_MAX) atomicMin(a.bad + a.stage, s_bad);
+    if (s_cnt[0]) atomicAdd(a.counters + 0, (unsigned long long)s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(a.counters + 1, (unsigned long long)s_cnt[1]);
+    if (s_cnt[2]) atomicAdd(a.counters + 2, (unsigned long long)s_cnt[2]);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -559,7 +544,7 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
 }
 
 #ifndef MHD_TY3
-#define MHD_TY3 5
+#define MHD_TY3 7
 #endif
 #ifndef MHD_TY2
 #define MHD_TY2 5
