@@ -74,9 +74,9 @@ struct StageSmem {
 #ifndef MHD_OCCW
 #define MHD_OCCW 2
 #endif
-template <int DIM, int TY, int WZ>
+template <int DIM, int TY, int REC>
 struct StageOcc {
-  static constexpr int value = DIM == 3 ? (WZ ? MHD_OCCW : MHD_OCC3) : (DIM == 2 ? 2 : 4);
+  static constexpr int value = DIM == 3 ? (REC == 2 ? MHD_OCCW : MHD_OCC3) : (DIM == 2 ? 2 : 4);
 };
 
 // One CTA: a 32 x TY cell tile (TY "cell warps", lane = x) plus one "edge warp", marching
@@ -91,8 +91,11 @@ struct StageOcc {
 // so every warp runs at most 3 face solves per plane and the per-plane barriers do not wait
 // on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
-template <int DIM, int NV, int RS, int TY, int WZ>
-__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value)) k_stage(StageArgs a) {
+template <int DIM, int NV, int RS, int TY, int REC>
+__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)) k_stage(StageArgs a) {
+  // REC: reconstruction, a compile-time choice (0 PLM minmod, 1 PLM MC, 2 WENO-Z)
+  constexpr bool WZ = REC == 2;
+  constexpr int LIM = REC == 0 ? 0 : 1;
   constexpr int G = WZ ? 3 : 2;  // reconstruction half-width: PLM 2, WENO-Z 3
   using S = StageSmem<DIM, NV, TY, G>;
   constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH, NT = S::NT;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
         convert_own(kb - 2, qA, false);
         convert_own(kb - 1, qB, false);
         convert_own(kb, qC, true);  // the counted conversion of plane kb
-        plm_cell<NV>(c.limiter, qA, qB, qC, qp, qm);
+        plm_cell<NV, LIM>(qA, qB, qC, qp, qm);
       }
       double wp[NV];
       to_normal<NV, 2>(qp, wp);  // Vpz is kept in the z normal frame
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
             fb = weno_cell<NV>(qm1, q0, q1, q2, q3, qp, qm);
           } else {  // cell k+1 from V(k..k+2); plane k+2 is first touched here
             convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
-            fb = plm_cell<NV>(c.limiter, q0, q1, q2, qp, qm);
+            fb = plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
           }
           double wp[NV];
           to_normal<NV, 2>(qp, wp);
@@ -324,8 +327,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, WZ>::value))
               qc[n] = base[0];
               qd[n] = base[s];
             }
-            plm_cell<NV>(c.limiter, qa, qb, qc, wl, tmp);       // left cell: V+
-            fb = plm_cell<NV>(c.limiter, qb, qc, qd, tmp, wr);  // right cell: V-
+            plm_cell<NV, LIM>(qa, qb, qc, wl, tmp);       // left cell: V+
+            fb = plm_cell<NV, LIM>(qb, qc, qd, tmp, wr);  // right cell: V-
           }
         }
         if (fb && cnt_right) atomicAdd(&s_cnt[1], 1);
@@ -524,10 +527,10 @@ __global__ void k_face_flux(const double* __restrict__ VL, const double* __restr
 // ---------------------------------------------------------------------------------------
 // host-side launchers (explicit instantiations)
 // ---------------------------------------------------------------------------------------
-template <int DIM, int NV, int RS, int TY, int WZ>
+template <int DIM, int NV, int RS, int TY, int REC>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
-  using S = StageSmem<DIM, NV, TY, WZ ? 3 : 2>;
-  auto kern = k_stage<DIM, NV, RS, TY, WZ>;
+  using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
+  auto kern = k_stage<DIM, NV, RS, TY, REC>;
   static bool attr_set = false;
   static size_t extra = 0;  // MHD_EXTRA_SMEM (bytes): measurement knob for the L1 carve-out
   if (!attr_set) {
@@ -552,28 +555,29 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
 #ifndef MHD_TYW3
 #define MHD_TYW3 5
 #endif
-template <int WZ>
+template <int REC>
 static cudaError_t launch_stage_w(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
   if (dim == 3) {
-    constexpr int TY3 = WZ ? MHD_TYW3 : MHD_TY3;
-    if (riemann) return launch_stage_t<3, 9, 1, TY3, WZ>(a, st);
-    return launch_stage_t<3, 9, 0, TY3, WZ>(a, st);
+    constexpr int TY3 = REC == 2 ? MHD_TYW3 : MHD_TY3;
+    if (riemann) return launch_stage_t<3, 9, 1, TY3, REC>(a, st);
+    return launch_stage_t<3, 9, 0, TY3, REC>(a, st);
   }
   if (dim == 2) {
-    if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2, WZ>(a, st);
-    return launch_stage_t<2, 9, 0, MHD_TY2, WZ>(a, st);
+    if (riemann) return launch_stage_t<2, 9, 1, MHD_TY2, REC>(a, st);
+    return launch_stage_t<2, 9, 0, MHD_TY2, REC>(a, st);
   }
   if (nv == 9) {
-    if (riemann) return launch_stage_t<1, 9, 1, 1, WZ>(a, st);
-    return launch_stage_t<1, 9, 0, 1, WZ>(a, st);
+    if (riemann) return launch_stage_t<1, 9, 1, 1, REC>(a, st);
+    return launch_stage_t<1, 9, 0, 1, REC>(a, st);
   }
-  if (riemann) return launch_stage_t<1, 8, 1, 1, WZ>(a, st);
-  return launch_stage_t<1, 8, 0, 1, WZ>(a, st);
+  if (riemann) return launch_stage_t<1, 8, 1, 1, REC>(a, st);
+  return launch_stage_t<1, 8, 0, 1, REC>(a, st);
 }
 
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st) {
-  // limiter 2 = WENO-Z (ghost width 3); 0/1 = PLM minmod/MC (runtime branch inside the kernel)
-  if (a.c.limiter == 2) return launch_stage_w<1>(dim, nv, riemann, a, st);
+  // the reconstruction is a template parameter: 0 PLM minmod, 1 PLM MC, 2 WENO-Z (ghost width 3)
+  if (a.c.limiter == 2) return launch_stage_w<2>(dim, nv, riemann, a, st);
+  if (a.c.limiter == 1) return launch_stage_w<1>(dim, nv, riemann, a, st);
   return launch_stage_w<0>(dim, nv, riemann, a, st);
 }
 
@@ -581,10 +585,10 @@ int stage_tile_rows(int dim, int limiter) {
   return dim == 3 ? (limiter == 2 ? MHD_TYW3 : MHD_TY3) : (dim == 2 ? MHD_TY2 : 1);
 }
 
-template <int DIM, int NV, int RS, int TY, int WZ>
+template <int DIM, int NV, int RS, int TY, int REC>
 static int ctas_per_sm_t() {
-  using S = StageSmem<DIM, NV, TY, WZ ? 3 : 2>;
-  auto kern = k_stage<DIM, NV, RS, TY, WZ>;
+  using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
+  auto kern = k_stage<DIM, NV, RS, TY, REC>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, S::NT, S::bytes) != cudaSuccess) n = 1;
@@ -593,12 +597,12 @@ static int ctas_per_sm_t() {
 
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter) {
   if (limiter == 2) {
-    if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TYW3, 1>() : ctas_per_sm_t<3, 9, 0, MHD_TYW3, 1>();
-    if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 1>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 1>();
+    if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TYW3, 2>() : ctas_per_sm_t<3, 9, 0, MHD_TYW3, 2>();
+    if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 2>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 2>();
     return 1;
   }
-  if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3, 0>() : ctas_per_sm_t<3, 9, 0, MHD_TY3, 0>();
-  if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 0>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 0>();
+  if (dim == 3) return riemann ? ctas_per_sm_t<3, 9, 1, MHD_TY3, 1>() : ctas_per_sm_t<3, 9, 0, MHD_TY3, 1>();
+  if (dim == 2) return riemann ? ctas_per_sm_t<2, 9, 1, MHD_TY2, 1>() : ctas_per_sm_t<2, 9, 0, MHD_TY2, 1>();
   return 1;
 }
 
