@@ -388,10 +388,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         a.Uout[off + f * fstride] = v;
       }
     }
-    // ---- advance the plane window (3D)
+    // ---- advance the plane window (3D).  No barrier before the load: the update reads only
+    // the flux buffers, and every read of Vc (the face jobs) finished at the barrier above;
+    // the barrier after it also orders this update before the next plane's flux writes.
     if constexpr (DIM == 3) {
       if (k + 1 < ke) {
-        __syncthreads();
         load_plane(k + 1, false);
         __syncthreads();
       }
