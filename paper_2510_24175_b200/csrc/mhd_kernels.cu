@@ -53,6 +53,10 @@ __device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("pre
 
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
+#ifndef MHD_JOB_UNROLL
+#define MHD_JOB_UNROLL 1
+#endif
+constexpr int kJobUnroll = MHD_JOB_UNROLL;  // face-job loop unrolling (1: one face-solve instance)
 #ifndef MHD_OCC3
 #define MHD_OCC3 2
 #endif
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         if (full && a.mode != 0) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
       }
     }
-#pragma unroll 1
+#pragma unroll kJobUnroll
     for (int job = 0; job <= 3; ++job) {
       // ---- select the face of this job (warp-uniform activity)
       int d = 0, row = ty, col = tx;
