@@ -36,7 +36,7 @@ class Config(C.Structure):
                 ("bc_lo", C.c_int32 * 3), ("bc_hi", C.c_int32 * 3), ("gamma", C.c_double),
                 ("cfl", C.c_double), ("limiter", C.c_int32), ("riemann", C.c_int32),
                 ("glm", C.c_int32), ("stepper", C.c_int32), ("glm_alpha", C.c_double),
-                ("p_floor", C.c_double)]
+                ("p_floor", C.c_double), ("ct", C.c_int32), ("pad2_", C.c_int32)]
 
 
 class Counters(C.Structure):
@@ -66,6 +66,8 @@ def lib():
         L.orc_fast_speed.restype = C.c_double
         L.orc_limited_slope.argtypes = [C.c_int32, C.c_double, C.c_double]
         L.orc_limited_slope.restype = C.c_double
+        L.orc_ct_divb.argtypes = [C.POINTER(Config), _D, _D]
+        L.orc_ct_divb.restype = C.c_int
         L.orc_wenoz.argtypes = [C.c_double] * 5
         L.orc_wenoz.restype = C.c_double
         L.orc_face_flux.argtypes = [C.POINTER(Config), _D, _D, C.c_double, _D]
@@ -109,6 +111,7 @@ def make_config(problem) -> Config:
     c.stepper = int(getattr(problem, "stepper", 0))
     c.glm_alpha = float(problem.glm_alpha)
     c.p_floor = float(problem.p_floor)
+    c.ct = int(getattr(problem, "ct", 0))
     return c
 
 
@@ -175,6 +178,17 @@ def total_energy(gamma, V):
 
 def fast_speed(gamma, rho, p, bn, bt1, bt2):
     return lib().orc_fast_speed(gamma, rho, p, bn, bt1, bt2)
+
+
+def ct_divb(problem, U):
+    """discrete div b of a CT state (face fields 5..7), per interior cell [nz][ny][nx]."""
+    cfg = make_config(problem)
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    out = np.zeros(U.shape[1:], dtype=np.float64)
+    rc = lib().orc_ct_divb(C.byref(cfg), _ptr(U), _ptr(out))
+    if rc:
+        raise OracleError(rc, Counters())
+    return out
 
 
 def wenoz(a, b, c, d, e):

@@ -66,6 +66,9 @@ static int make_grid(const orc_config* c, grid_t* G) {
     nact += G->act[d];
   }
   if (nact == 0) return ORC_E_ARG;
+  if (c->ct && (nact != 3 || c->glm)) return ORC_E_ARG;
+  for (int d = 0; d < 3 && c->ct; ++d)
+    if (c->bc_lo[d] != 0 || c->bc_hi[d] != 0) return ORC_E_ARG;
   G->nvar = 8 + (c->glm ? 1 : 0);
   return ORC_OK;
 }
@@ -625,6 +628,234 @@ int orc_stage(const orc_config* c, const double* U, double* Uout, double dt, dou
 }
 
 /* ------------------------------------------------------------------------ */
+/* Constrained transport (the paper's weak-scaling div-B */
+/* method, refs Evans & Hawley 1988, Londrillo & Del      */
+/* Zanna 2004; reading R32).  3D, periodic, no GLM.  U fields 5..7 hold the   */
+/* face-centred b_x at x-face i-1/2, b_y at y-face j-1/2, b_z at z-face k-1/2 */
+/* of cell (i,j,k).  Per stage:                                              */
+/*  1. cell-centred B = 0.5 (b(face -1/2) + b(face +1/2)) per component;     */
+/*  2. c.3 cons->prim of (rho, m, E, B_cell);                                */
+/*  3. reconstruction (c.5 / R31) of the primitives along each direction;    */
+/*  4. at face i-1/2 the normal field of both states is the face value b;    */
+/*     face solve c.6-c.10 without GLM (Bm = b): fluxes of rho, m, E and the */
+/*     face EMFs (E = -v x B): x-face Ez = -F[By], Ey = F[Bz]; y-face        */
+/*     Ex = -F[Bz], Ez = F[Bx]; z-face Ey = -F[Bx], Ex = F[By];              */
+/*  5. edge EMFs, arithmetic 4-face average, e.g. at edge      */
+/*     (i-1/2, j-1/2): Ez = 0.25 (((Ezx(i,j-1) + Ezx(i,j)) + Ezy(i-1,j)) +   */
+/*     Ezy(i,j)) (faces of the first direction of the cyclic pair first);   */
+/*  6. S(U): rho, m, E by c.11; face fields by Stokes,                        */
+/*     bx -= ly (Ez(j+1/2) - Ez(j-1/2)) - lz (Ey(k+1/2) - Ey(k-1/2)),        */
+/*     by -= lz (Ex(k+1/2) - Ex(k-1/2)) - lx (Ez(i+1/2) - Ez(i-1/2)),        */
+/*     bz -= lx (Ey(i+1/2) - Ey(i-1/2)) - ly (Ex(j+1/2) - Ex(j-1/2)),        */
+/*     each as b - ((la dEa) - (lb dEb)).  The discrete divergence of b is    */
+/*     unchanged up to rounding.  N faces per periodic line (counters).       */
+/* ------------------------------------------------------------------------ */
+#define CTI(i, n) ((((i) % (n)) + (n)) % (n))
+
+static size_t ct_at(const grid_t* G, int f, int64_t i, int64_t j, int64_t k) {
+  return (((size_t)f * G->n[2] + CTI(k, G->n[2])) * G->n[1] + CTI(j, G->n[1])) * G->n[0] + CTI(i, G->n[0]);
+}
+
+/* cell-centred conservative vector (B from the face average) of cell (i,j,k) */
+static void ct_cell_cons(const grid_t* G, const double* U, int64_t i, int64_t j, int64_t k, double* w) {
+  for (int f = 0; f < 5; ++f) w[f] = U[ct_at(G, f, i, j, k)];
+  w[5] = 0.5 * (U[ct_at(G, 5, i, j, k)] + U[ct_at(G, 5, i + 1, j, k)]);
+  w[6] = 0.5 * (U[ct_at(G, 6, i, j, k)] + U[ct_at(G, 6, i, j + 1, k)]);
+  w[7] = 0.5 * (U[ct_at(G, 7, i, j, k)] + U[ct_at(G, 7, i, j, k + 1)]);
+}
+
+int orc_ct_divb(const orc_config* c, const double* U, double* out) {
+  grid_t G;
+  int rc = make_grid(c, &G);
+  if (rc) return rc;
+  for (int64_t k = 0; k < G.n[2]; ++k)
+    for (int64_t j = 0; j < G.n[1]; ++j)
+      for (int64_t i = 0; i < G.n[0]; ++i)
+        out[(k * G.n[1] + j) * G.n[0] + i] =
+            ((U[ct_at(&G, 5, i + 1, j, k)] - U[ct_at(&G, 5, i, j, k)]) / G.dx[0] +
+             (U[ct_at(&G, 6, i, j + 1, k)] - U[ct_at(&G, 6, i, j, k)]) / G.dx[1]) +
+            (U[ct_at(&G, 7, i, j, k + 1)] - U[ct_at(&G, 7, i, j, k)]) / G.dx[2];
+  return ORC_OK;
+}
+
+static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, double* Out, const double lam[3],
+                       int stage, orc_counters* cnt) {
+  const int64_t nx = G->n[0], ny = G->n[1], nz = G->n[2];
+  const size_t ncell = (size_t)nx * ny * nz;
+  const int wz = c->limiter == 2;
+
+  /* validity of the stage input (R16) */
+  int64_t first_bad = INT64_MAX;
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        double u[8];
+        for (int f = 0; f < 8; ++f) u[f] = Uin[ct_at(G, f, i, j, k)];
+        if (bad_cell(u, 8) && interior_linear(G, i, j, k) < first_bad) first_bad = interior_linear(G, i, j, k);
+      }
+  if (first_bad != INT64_MAX) {
+    if (cnt->bad_stage < 0) {
+      cnt->bad_stage = stage;
+      cnt->first_bad_cell = first_bad;
+    }
+    return ORC_E_UNPHYSICAL;
+  }
+
+  /* 1-2: cell-centred primitives */
+  double* V = (double*)calloc(8 * ncell, sizeof(double));
+  int64_t floors = 0;
+#pragma omp parallel for reduction(+ : floors) schedule(static)
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        double w[8], v[8];
+        ct_cell_cons(G, Uin, i, j, k, w);
+        floors += orc_cons2prim(c, w, v);
+        for (int f = 0; f < 8; ++f) V[ct_at(G, f, i, j, k)] = v[f];
+      }
+  cnt->p_floors += floors;
+
+  /* 3-4: per direction, reconstruction and the face solve at face i-1/2 of every cell */
+  double* F[3];
+  int64_t fallbacks = 0, to_hll = 0;
+  for (int d = 0; d < 3; ++d) {
+    F[d] = (double*)calloc(8 * ncell, sizeof(double));
+    double* Vp = (double*)calloc(8 * ncell, sizeof(double));
+    double* Vm = (double*)calloc(8 * ncell, sizeof(double));
+    int64_t o[3] = {0, 0, 0};
+    o[d] = 1;
+#pragma omp parallel for reduction(+ : fallbacks) schedule(static)
+    for (int64_t k = 0; k < nz; ++k)
+      for (int64_t j = 0; j < ny; ++j)
+        for (int64_t i = 0; i < nx; ++i) {
+          double qp[8], qm[8], q0[8];
+          for (int f = 0; f < 8; ++f) {
+            const double qa = V[ct_at(G, f, i - o[0], j - o[1], k - o[2])];
+            const double qb = V[ct_at(G, f, i, j, k)];
+            const double qc = V[ct_at(G, f, i + o[0], j + o[1], k + o[2])];
+            q0[f] = qb;
+            if (wz) {
+              const double qaa = V[ct_at(G, f, i - 2 * o[0], j - 2 * o[1], k - 2 * o[2])];
+              const double qcc = V[ct_at(G, f, i + 2 * o[0], j + 2 * o[1], k + 2 * o[2])];
+              qp[f] = orc_wenoz(qaa, qa, qb, qc, qcc);
+              qm[f] = orc_wenoz(qcc, qc, qb, qa, qaa);
+            } else {
+              const double s = orc_limited_slope(c->limiter, qb - qa, qc - qb);
+              qp[f] = qb + 0.5 * s;
+              qm[f] = qb - 0.5 * s;
+            }
+          }
+          if (!(qp[0] > 0.0 && qm[0] > 0.0 && qp[4] > 0.0 && qm[4] > 0.0)) {
+            for (int f = 0; f < 8; ++f) qp[f] = qm[f] = q0[f];
+            fallbacks += 1;
+          }
+          for (int f = 0; f < 8; ++f) {
+            Vp[ct_at(G, f, i, j, k)] = qp[f];
+            Vm[ct_at(G, f, i, j, k)] = qm[f];
+          }
+        }
+#pragma omp parallel for reduction(+ : to_hll) schedule(static)
+    for (int64_t k = 0; k < nz; ++k)
+      for (int64_t j = 0; j < ny; ++j)
+        for (int64_t i = 0; i < nx; ++i) {
+          double vl[8], vr[8], wl[8], wr[8], fn[8], fx[8];
+          for (int f = 0; f < 8; ++f) {
+            vl[f] = Vp[ct_at(G, f, i - o[0], j - o[1], k - o[2])];
+            vr[f] = Vm[ct_at(G, f, i, j, k)];
+          }
+          const double b = Uin[ct_at(G, 5 + d, i, j, k)]; /* the staggered normal field of face i-1/2 */
+          vl[5 + d] = b;
+          vr[5 + d] = b;
+          to_normal(d, 8, vl, wl);
+          to_normal(d, 8, vr, wr);
+          to_hll += orc_face_flux(c, wl, wr, 0.0, fn);
+          from_normal(d, 8, fn, fx);
+          for (int f = 0; f < 8; ++f) F[d][ct_at(G, f, i, j, k)] = fx[f];
+        }
+    free(Vp);
+    free(Vm);
+  }
+  cnt->plm_fallbacks += fallbacks;
+  cnt->hlld_to_hll += to_hll;
+
+  /* 5: edge EMFs.  Ez[i,j,k] at edge (i-1/2, j-1/2, k); Ex[i,j,k] at (i, j-1/2, k-1/2);
+   * Ey[i,j,k] at (i-1/2, j, k-1/2).  Face EMFs from the induction fluxes (step 4). */
+  double* Ez = (double*)calloc(ncell, sizeof(double));
+  double* Ex = (double*)calloc(ncell, sizeof(double));
+  double* Ey = (double*)calloc(ncell, sizeof(double));
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        const size_t q = ct_at(G, 0, i, j, k);
+        /* Ez: x faces (i-1/2) of rows j-1, j; y faces (j-1/2) of columns i-1, i */
+        const double ezx0 = -F[0][ct_at(G, 6, i, j - 1, k)], ezx1 = -F[0][ct_at(G, 6, i, j, k)];
+        const double ezy0 = F[1][ct_at(G, 5, i - 1, j, k)], ezy1 = F[1][ct_at(G, 5, i, j, k)];
+        Ez[q] = 0.25 * (((ezx0 + ezx1) + ezy0) + ezy1);
+        /* Ex: y faces (j-1/2) of planes k-1, k; z faces (k-1/2) of rows j-1, j */
+        const double exy0 = -F[1][ct_at(G, 7, i, j, k - 1)], exy1 = -F[1][ct_at(G, 7, i, j, k)];
+        const double exz0 = F[2][ct_at(G, 6, i, j - 1, k)], exz1 = F[2][ct_at(G, 6, i, j, k)];
+        Ex[q] = 0.25 * (((exy0 + exy1) + exz0) + exz1);
+        /* Ey: z faces (k-1/2) of columns i-1, i; x faces (i-1/2) of planes k-1, k */
+        const double eyz0 = -F[2][ct_at(G, 5, i - 1, j, k)], eyz1 = -F[2][ct_at(G, 5, i, j, k)];
+        const double eyx0 = F[0][ct_at(G, 7, i, j, k - 1)], eyx1 = F[0][ct_at(G, 7, i, j, k)];
+        Ey[q] = 0.25 * (((eyz0 + eyz1) + eyx0) + eyx1);
+      }
+
+  /* 6: update */
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nz; ++k)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        for (int f = 0; f < 5; ++f) { /* c.11 */
+          double r = lam[0] * (F[0][ct_at(G, f, i + 1, j, k)] - F[0][ct_at(G, f, i, j, k)]);
+          r = r + lam[1] * (F[1][ct_at(G, f, i, j + 1, k)] - F[1][ct_at(G, f, i, j, k)]);
+          r = r + lam[2] * (F[2][ct_at(G, f, i, j, k + 1)] - F[2][ct_at(G, f, i, j, k)]);
+          const size_t q = ct_at(G, f, i, j, k);
+          Out[q] = Uin[q] - r;
+        }
+        const size_t e = ct_at(G, 0, i, j, k);
+        const double rbx = lam[1] * (Ez[ct_at(G, 0, i, j + 1, k)] - Ez[e]) - lam[2] * (Ey[ct_at(G, 0, i, j, k + 1)] - Ey[e]);
+        const double rby = lam[2] * (Ex[ct_at(G, 0, i, j, k + 1)] - Ex[e]) - lam[0] * (Ez[ct_at(G, 0, i + 1, j, k)] - Ez[e]);
+        const double rbz = lam[0] * (Ey[ct_at(G, 0, i + 1, j, k)] - Ey[e]) - lam[1] * (Ex[ct_at(G, 0, i, j + 1, k)] - Ex[e]);
+        Out[ct_at(G, 5, i, j, k)] = Uin[ct_at(G, 5, i, j, k)] - rbx;
+        Out[ct_at(G, 6, i, j, k)] = Uin[ct_at(G, 6, i, j, k)] - rby;
+        Out[ct_at(G, 7, i, j, k)] = Uin[ct_at(G, 7, i, j, k)] - rbz;
+      }
+  free(V);
+  for (int d = 0; d < 3; ++d) free(F[d]);
+  free(Ez);
+  free(Ex);
+  free(Ey);
+  return ORC_OK;
+}
+
+/* one RK step with CT (R30 weights, the same combination for every field) */
+static int step_ct(const orc_config* c, const grid_t* G, double* U, const double lam[3], orc_counters* cnt) {
+  const size_t n = 8 * (size_t)G->n[0] * G->n[1] * G->n[2];
+  double* Ua = (double*)calloc(n, sizeof(double));
+  double* Ub = (double*)calloc(n, sizeof(double));
+  int rc = stage_op_ct(c, G, U, Ua, lam, 1, cnt); /* U1 = S(U^n) */
+  if (rc == ORC_OK && c->stepper == 0) {
+    rc = stage_op_ct(c, G, Ua, Ub, lam, 2, cnt);
+    if (rc == ORC_OK)
+      for (size_t q = 0; q < n; ++q) U[q] = 0.5 * (U[q] + Ub[q]);
+  } else if (rc == ORC_OK) {
+    const double a2 = 0.75, b2 = 0.25, a3 = 1.0 / 3.0, b3 = 2.0 / 3.0;
+    rc = stage_op_ct(c, G, Ua, Ub, lam, 2, cnt);
+    if (rc == ORC_OK) {
+      for (size_t q = 0; q < n; ++q) Ub[q] = (a2 * U[q]) + (b2 * Ub[q]);
+      rc = stage_op_ct(c, G, Ub, Ua, lam, 3, cnt);
+    }
+    if (rc == ORC_OK)
+      for (size_t q = 0; q < n; ++q) U[q] = (a3 * U[q]) + (b3 * Ua[q]);
+  }
+  free(Ua);
+  free(Ub);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
 /* c.11-c.12: one RK step and the GLM damping                                 */
 /*   SSP-RK2 (Heun, R2):  U* = S(U^n); U^{n+1} = 0.5 (U^n + S(U*))             */
 /*   SSP-RK3 (Shu & Osher 1988; the paper's integrator; reading  */
@@ -646,6 +877,7 @@ int orc_step(const orc_config* c, double* U, double dt, double ch, orc_counters*
     if (G.act[d] && G.dx[d] < dxmin) dxmin = G.dx[d];
   }
   const double damp = exp(-((c->glm_alpha * ch) * dt) / dxmin);
+  if (c->ct) return step_ct(c, &G, U, lam, cnt);
 
   const size_t np = padded_size(&G);
   double* Un = (double*)calloc(np, sizeof(double));
@@ -719,6 +951,7 @@ int orc_compute_dt(const orc_config* c, const double* U, double* dt, double* ch,
         const size_t lin = (size_t)interior_linear(&G, i, j, k);
         double u[9], v[9];
         for (int f = 0; f < nvar; ++f) u[f] = U[(size_t)f * ncell + lin];
+        if (c->ct) ct_cell_cons(&G, U, i, j, k, u); /* CT: B from the face average (R32) */
         if (bad_cell(u, nvar)) {
           if ((int64_t)lin < first_bad) first_bad = (int64_t)lin;
           continue;

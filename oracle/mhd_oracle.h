@@ -39,6 +39,9 @@ typedef struct {
   int32_t stepper;     /* 0 SSP-RK2 (Heun, R2), 1 SSP-RK3 (Shu-Osher) */
   double glm_alpha;    /* 0.1 (R12) */
   double p_floor;      /* 1e-12 (R16) */
+  int32_t ct;          /* 1: constrained transport: U fields 5..7 are the
+                          face-centred b_x (face i-1/2), b_y (j-1/2), b_z (k-1/2); 3D periodic, glm 0 */
+  int32_t pad2_;
 } orc_config;
 
 typedef struct {
@@ -52,6 +55,9 @@ typedef struct {
 
 /* counters must be reset by the caller before the first call (bad_stage = first_bad_cell = -1) */
 void orc_counters_reset(orc_counters* cnt);
+/* CT: discrete divergence sum_d (b_d(i+1) - b_d(i))/dx_d of the face field of interior U, per cell
+ * (test helper for the div B pin; out has ncell entries). */
+int orc_ct_divb(const orc_config* c, const double* U, double* out);
 /* c.3: conservative -> primitive for one cell. Returns 1 if p was floored. */
 int orc_cons2prim(const orc_config* c, const double* U, double* V);
 /* c.4 energy of a primitive state (used by the tests for prim->cons round trips). */

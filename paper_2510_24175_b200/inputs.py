@@ -48,6 +48,7 @@ class Problem:
     p_floor: float = 1e-12
     t_end: float = 0.0
     stepper: int = 0  # 0 SSP-RK2 (north star), 1 SSP-RK3 (the paper's RK3)
+    ct: int = 0       # 1 constrained transport: fields 5..7 face-centred, glm 0
 
     @property
     def nvar(self) -> int:
@@ -254,6 +255,63 @@ def cpa_3d_ic(p: Problem, z_range=None) -> np.ndarray:
     rho, V, pr, B = cpa_3d_fields(p, 0.0, z_range=z_range)
     sub = p if z_range is None else p.replace(n=(p.n[0], p.n[1], z_range[1] - z_range[0]))
     return prim_to_cons_ic(sub, rho, V[0], V[1], V[2], pr, B[0], B[1], B[2])
+
+
+def ct_problem(p: Problem) -> Problem:
+    """the same problem with constrained transport instead of GLM (3D periodic only)"""
+    return p.replace(ct=1, glm=0)
+
+
+def _edge_coords(p: Problem, stag):
+    """meshgrid of cell centres shifted by -1/2 cell along the axes in stag (edge / face centres)"""
+    cs = []
+    for d in range(3):
+        dx = (p.hi[d] - p.lo[d]) / p.n[d]
+        c = p.lo[d] + (np.arange(p.n[d], dtype=np.float64) + (0.0 if d in stag else 0.5)) * dx
+        cs.append(c)
+    Z, Y, X = np.meshgrid(cs[2], cs[1], cs[0], indexing="ij")
+    return X, Y, Z
+
+
+def ct_faces_from_potential(p: Problem, A_fn, b0=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """face-centred field b = curl A from the edge-centred vector potential A_fn(X, Y, Z) -> (Ax, Ay, Az)
+    (discretely divergence-free to rounding), plus a uniform field b0.  Returns [3][nz][ny][nx]:
+    b_x at x-face i-1/2, b_y at y-face j-1/2, b_z at z-face k-1/2 of cell (i,j,k)."""
+    dx = [(p.hi[d] - p.lo[d]) / p.n[d] for d in range(3)]
+    Ax = A_fn(*_edge_coords(p, (1, 2)))[0]  # at (x_i, y_{j-1/2}, z_{k-1/2})
+    Ay = A_fn(*_edge_coords(p, (0, 2)))[1]  # at (x_{i-1/2}, y_j, z_{k-1/2})
+    Az = A_fn(*_edge_coords(p, (0, 1)))[2]  # at (x_{i-1/2}, y_{j-1/2}, z_k)
+    up = lambda a, ax: np.roll(a, -1, axis=ax)  # value at index + 1 (periodic); axes: 0 z, 1 y, 2 x
+    bx = (up(Az, 1) - Az) / dx[1] - (up(Ay, 0) - Ay) / dx[2] + b0[0]
+    by = (up(Ax, 0) - Ax) / dx[2] - (up(Az, 2) - Az) / dx[0] + b0[1]
+    bz = (up(Ay, 2) - Ay) / dx[0] - (up(Ax, 1) - Ax) / dx[1] + b0[2]
+    return np.stack([bx, by, bz])
+
+
+def ct_state(p: Problem, rho, V, pr, bface) -> np.ndarray:
+    """CT conservative state: rho, m, E with the cell-centred B = face average, and the face fields."""
+    bc = [0.5 * (bface[0] + np.roll(bface[0], -1, axis=2)), 0.5 * (bface[1] + np.roll(bface[1], -1, axis=1)),
+          0.5 * (bface[2] + np.roll(bface[2], -1, axis=0))]
+    U = prim_to_cons_ic(p, rho, V[0], V[1], V[2], pr, bc[0], bc[1], bc[2])
+    U[5:8] = bface
+    return U
+
+
+def cpa_3d_ct_ic(p: Problem, amp: float = 0.1) -> np.ndarray:
+    """3D CPA with face-centred b = B_par n + curl A_w, A_w = (amp/|k|)(sin phi t1 + cos phi t2)
+    (curl A_w = amp (sin phi t1 + cos phi t2) for phi = k.x, k = 2pi(1,1,1))."""
+    s3 = math.sqrt(3.0)
+    n = np.array([1.0, 1.0, 1.0]) / s3
+    t1 = np.array([1.0, -1.0, 0.0]) / math.sqrt(2.0)
+    t2 = np.array([1.0, 1.0, -2.0]) / math.sqrt(6.0)
+    kabs = 2.0 * math.pi * s3
+
+    def A(X, Y, Z):
+        ph = 2.0 * math.pi * (X + Y + Z)
+        return [(amp / kabs) * (np.sin(ph) * t1[c] + np.cos(ph) * t2[c]) for c in range(3)]
+    bface = ct_faces_from_potential(p, A, b0=tuple(n))
+    rho, V, pr, _ = cpa_3d_fields(p, 0.0, amp)
+    return ct_state(p, rho, V, pr, bface)
 
 
 def with_noise(U: np.ndarray, p: Problem, amp: float = 1e-3, seed: int = 2510) -> np.ndarray:

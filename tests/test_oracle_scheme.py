@@ -350,3 +350,66 @@ def test_wenoz_3d_ot_conservation_and_embedding():
         o1.step(dt, ch)
         o3.step(dt, ch)
     assert np.array_equal(np.broadcast_to(o1.U, (9, 4, 4, 64)), o3.U)
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) row 4: constrained transport (R32)
+# ---------------------------------------------------------------------------------------------
+def _random_ct_state(p, seed=7):
+    rng = np.random.default_rng(seed)
+    modes = [(rng.integers(1, 3, 3), rng.normal(size=3), rng.uniform(0, 6.28)) for _ in range(3)]
+
+    def A(X, Y, Z):
+        out = [np.zeros_like(X) for _ in range(3)]
+        for kv, amp, ph in modes:
+            arg = 2 * math.pi * (kv[0] * X + kv[1] * Y + kv[2] * Z) + ph
+            for c in range(3):
+                out[c] = out[c] + 0.05 * amp[c] * np.sin(arg)
+        return out
+    bface = I.ct_faces_from_potential(p, A, b0=(0.3, -0.2, 0.5))
+    X, Y, Z = I.mesh(p)
+    rho = 1.0 + 0.2 * np.sin(2 * math.pi * (X + 2 * Y))
+    V = [0.3 * np.cos(2 * math.pi * Z), 0.2 * np.sin(2 * math.pi * X), -0.1 + 0 * X]
+    return I.ct_state(p, rho, V, 1.0 + 0.1 * np.cos(2 * math.pi * Y), bface)
+
+
+@pytest.mark.parametrize("limiter,stepper", [(I.MC, I.RK2), (I.WENOZ, I.RK3)])
+def test_ct_preserves_discrete_divergence(limiter, stepper):
+    """CT's defining property (Evans & Hawley 1988): the face-difference divergence of b is kept
+    at its initial value to rounding, here for a field built as the discrete curl of a random
+    vector potential (div b = 0 to ~1e-15 initially)."""
+    p = I.orszag_tang_3d(12, limiter=limiter).replace(ct=1, glm=0, stepper=stepper)
+    U0 = _random_ct_state(p)
+    d0 = np.abs(oracle.ct_divb(p, U0)).max()
+    assert d0 < 1e-12
+    o = oracle.Oracle(p, U0)
+    o.run(15)
+    d1 = np.abs(oracle.ct_divb(p, o.U)).max()
+    assert d1 < 1e-11, d1  # |b| ~ 1, dx = 1/12: a non-CT update gives O(1e-2)
+    # conservation: rho, m, E by the flux form; the total of every face component by Stokes
+    for f in range(8):
+        assert abs(o.U[f].sum() - U0[f].sum()) <= 1e-12 * max(np.abs(U0[f]).sum(), 1.0)
+
+
+def test_ct_uniform_state_is_exact_fixed_point():
+    p = I.orszag_tang_3d(8).replace(ct=1, glm=0)
+    U = I.ct_state(p, 1.3, [0.2, -0.1, 0.3], 0.7, np.stack([np.full((8, 8, 8), b) for b in (0.4, 0.5, -0.6)]))
+    o = oracle.Oracle(p, U)
+    o.run(3)
+    assert np.array_equal(o.U, U)
+
+
+@pytest.mark.slow
+def test_ct_cpa_3d_convergence():
+    """the paper's CPA with CT (its weak-scaling div-B method): second order on the
+    exact solution, div b stays at rounding."""
+    errs = []
+    for n in (8, 16, 32):
+        p = I.ct_problem(I.cpa_3d(n))
+        U0 = I.cpa_3d_ct_ic(p)
+        o = oracle.Oracle(p, U0)
+        o.run(10 ** 6, p.t_end)
+        errs.append(np.abs(o.U[6] - U0[6]).mean() / 0.1)
+        assert np.abs(oracle.ct_divb(p, o.U)).max() * (1.0 / n) < 1e-13
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert orders[-1] >= 1.8, (errs, orders)
