@@ -41,6 +41,8 @@ struct mhd_ctx {
   double* U0 = nullptr;  // U^n
   double* U1 = nullptr;  // U* (RK2) / U1 (RK3)
   double* U2 = nullptr;  // RK3 only: U2
+  double* ctV = nullptr;                          // CT scratch: primitives
+  double* ctF[3] = {nullptr, nullptr, nullptr};   // CT scratch: face fluxes
   size_t arr_elems = 0;
   unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..8] bad slots, [20] debug
   unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (the first 9 entries)
@@ -308,6 +310,34 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   return MHD_OK;
 }
 
+// one CT stage (mhd_ct.cu): prim, three face passes, update with the RK epilogue
+int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+  const StagePlan sp = stage_plan(c, stage);
+  mhd::CtArgs a;
+  a.Uin = sp.in;
+  a.Un = c->U0;
+  a.Uout = sp.out;
+  a.V = c->ctV;
+  for (int d = 0; d < 3; ++d) a.F[d] = c->ctF[d];
+  a.nx = c->nx;
+  a.ny = c->ny;
+  a.nz = c->nzl;
+  a.gz = c->gz;
+  a.stage = stage;
+  a.mode = sp.mode;
+  a.last = sp.last;
+  a.wa = sp.wa;
+  a.wb = sp.wb;
+  a.c = k;
+  a.counters = c->dbuf + 2;
+  a.bad = c->dbuf + 5;
+  const int pr = prof_begin(c, 0);
+  cudaError_t e = mhd::launch_ct_stage(c->scheme.riemann, a, c->nsm, c->stream);
+  prof_end(c, pr);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "ct stage %d: %s", stage, cudaGetErrorString(e));
+  return MHD_OK;
+}
+
 // dt / c_h maxima of U^n into dbuf[0..1], reduced over ranks; reads back dbuf. Synchronising.
 int reduce_and_read(mhd_ctx* c) {
   CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 2 * sizeof(unsigned long long), c->stream));
@@ -326,7 +356,7 @@ int reduce_and_read(mhd_ctx* c) {
   d.bad = c->dbuf + 5;
   if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
   const int pr = prof_begin(c, 1);
-  cudaError_t e = mhd::launch_dt(c->dim, c->nv, d, c->nsm, c->stream);
+  cudaError_t e = c->scheme.ct ? mhd::launch_ct_dt(d, c->nsm, c->stream) : mhd::launch_dt(c->dim, c->nv, d, c->nsm, c->stream);
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt launch: %s", cudaGetErrorString(e));
   unsigned long long* src = c->dbuf;
@@ -425,12 +455,15 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     c->scheme.riemann = MHD_RS_HLLD;
     c->scheme.glm = 1;
     c->scheme.stepper = MHD_RK2;
+    c->scheme.ct = 0;
+    c->scheme.reserved = 0;
     c->scheme.glm_alpha = 0.1;
     c->scheme.p_floor = 1e-12;
   }
   if ((c->scheme.limiter != MHD_LIM_MINMOD && c->scheme.limiter != MHD_LIM_MC && c->scheme.limiter != MHD_LIM_WENOZ) ||
       (c->scheme.riemann != MHD_RS_HLL && c->scheme.riemann != MHD_RS_HLLD) || (c->scheme.glm != 0 && c->scheme.glm != 1) ||
-      (c->scheme.stepper != MHD_RK2 && c->scheme.stepper != MHD_RK3) ||
+      (c->scheme.stepper != MHD_RK2 && c->scheme.stepper != MHD_RK3) || (c->scheme.ct != 0 && c->scheme.ct != 1) ||
+      (c->scheme.ct && (c->scheme.glm || c->dim != 3)) ||
       !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm)) {
     delete c;
     return MHD_E_ARG;
@@ -440,6 +473,14 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->nv = 8 + c->scheme.glm;
   c->rank = dist ? dist->rank : 0;
   c->nranks = dist ? dist->nranks : 1;
+  if (c->scheme.ct) {  // CT: periodic on every axis, one GPU (R32)
+    bool ok = c->nranks == 1;
+    for (int d = 0; d < 3; ++d) ok = ok && c->bc_lo[d] == MHD_BC_PERIODIC;
+    if (!ok) {
+      delete c;
+      return MHD_E_ARG;
+    }
+  }
   if (dist && dist->transport != MHD_TRANSPORT_NCCL && dist->transport != MHD_TRANSPORT_LOCAL) {
     delete c;
     return MHD_E_ARG;
@@ -499,6 +540,10 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   cudaError_t e3 = cudaMalloc(&c->dbuf, 24 * sizeof(unsigned long long));
   if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.stepper == MHD_RK3)
     e2 = cudaMalloc(&c->U2, c->arr_elems * sizeof(double));
+  if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.ct) {
+    e2 = cudaMalloc(&c->ctV, c->arr_elems * sizeof(double));
+    for (int d = 0; d < 3 && e2 == cudaSuccess; ++d) e2 = cudaMalloc(&c->ctF[d], c->arr_elems * sizeof(double));
+  }
   cudaError_t e4 = cudaMallocHost(&c->hbuf, 24 * sizeof(unsigned long long));
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
     mhd_destroy(c);
@@ -562,7 +607,7 @@ int mhd_local_box(const mhd_ctx* c, int64_t off[3], int64_t ext[3]) {
 
 int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
   if (!c || !bytes) return MHD_E_ARG;
-  *bytes = (c->U2 ? 3 : 2) * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
+  *bytes = ((c->U2 ? 3 : 2) + (c->ctV ? 4 : 0)) * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
   return MHD_OK;
 }
 
@@ -583,8 +628,10 @@ int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
   }
   cudaError_t e = mhd::launch_pack(src, c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, 1, c->nsm, c->stream);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "pack: %s", cudaGetErrorString(e));
+  // (CT: the stored 5..7 are face fields, the pressure check of the cell-centred state is left
+  // to the first mhd_compute_dt, which floors and counts like every stage)
   e = mhd::launch_validate(c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, c->zoff, c->gamma - 1.0, c->dbuf + 5, c->nsm,
-                           c->stream);
+                           c->stream, c->scheme.ct ? 0 : 1);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "validate: %s", cudaGetErrorString(e));
   CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 5, c->dbuf + 5, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                     c->stream));
@@ -651,6 +698,13 @@ int mhd_step(mhd_ctx* c, double dt) {
   }
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
+  if (c->scheme.ct) {
+    for (int stage = 1; stage <= nstages(c); ++stage)
+      if ((rc = run_ct_stage(c, stage, k))) return rc;
+    c->ch_valid = false;
+    c->diag.steps += 1;
+    return MHD_OK;
+  }
   for (int stage = 1; stage <= nstages(c); ++stage) {
     double* U = stage_plan(c, stage).in;
     if ((rc = fill_z_ghosts_local(c, U))) return rc;
@@ -766,6 +820,9 @@ void mhd_destroy(mhd_ctx* c) {
   if (c->U0) cudaFree(c->U0);
   if (c->U1) cudaFree(c->U1);
   if (c->U2) cudaFree(c->U2);
+  if (c->ctV) cudaFree(c->ctV);
+  for (int d = 0; d < 3; ++d)
+    if (c->ctF[d]) cudaFree(c->ctF[d]);
   if (c->dbuf) cudaFree(c->dbuf);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -1,0 +1,240 @@
+// mhd_ct.cu — constrained transport path (R32).
+//
+// The paper's weak-scaling runs keep div B = 0 with constrained transport (
+// Evans & Hawley 1988, Londrillo & Del Zanna 2004).  State: rho, m, E cell-centred, b_x / b_y /
+// b_z on the x / y / z faces (face i-1/2 / j-1/2 / k-1/2 of cell (i,j,k)), 3D periodic, one GPU.
+// Per RK stage three kernels:
+//   k_ct_prim    cell-centred B = face average, cons->prim -> V (8 fields)
+//   k_ct_face<D> reconstruction along D, normal field = the face value, face solve -> F_D (the
+//                induction entries are the face EMFs)
+//   k_ct_update  rho, m, E by the flux divergence; b by Stokes with edge EMFs averaged from the
+//                four adjacent face EMFs (arithmetic); the RK epilogue.
+// The arithmetic of every step is the oracle's (oracle/mhd_oracle.c stage_op_ct) operation for
+// operation (built with --fmad=false), so the two agree bitwise.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "mhd_device.cuh"
+#include "mhd_kernels.h"
+
+namespace mhd {
+
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+struct CtIdx {
+  int nx, ny, nz, gz;
+  size_t fs, ps;  // field stride (nx*ny), plane stride (8*fs)
+  __device__ size_t at(int f, int i, int j, int k) const {
+    return (size_t)(wrapi(k, nz) + gz) * ps + (size_t)f * fs + (size_t)wrapi(j, ny) * nx + wrapi(i, nx);
+  }
+};
+
+__device__ __forceinline__ void ct_cell_cons(const double* __restrict__ U, const CtIdx& X, int i, int j, int k,
+                                             double* w) {
+#pragma unroll
+  for (int f = 0; f < 5; ++f) w[f] = __ldg(U + X.at(f, i, j, k));
+  w[5] = 0.5 * (__ldg(U + X.at(5, i, j, k)) + __ldg(U + X.at(5, i + 1, j, k)));
+  w[6] = 0.5 * (__ldg(U + X.at(6, i, j, k)) + __ldg(U + X.at(6, i, j + 1, k)));
+  w[7] = 0.5 * (__ldg(U + X.at(7, i, j, k)) + __ldg(U + X.at(7, i, j, k + 1)));
+}
+
+// 1-2: cell-centred primitives of every cell (V uses the same padded layout, ghost planes unused)
+__global__ void __launch_bounds__(256) k_ct_prim(CtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  int floors = 0;
+  unsigned long long bad = ULLONG_MAX;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    double u[8], w[8], v[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) u[f] = __ldg(a.Uin + X.at(f, i, j, k));
+    if (bad_state<8>(u)) bad = min(bad, (unsigned long long)q);
+    ct_cell_cons(a.Uin, X, i, j, k, w);
+    floors += cons2prim<8>(w, v, a.c.gm1, a.c.p_floor) ? 1 : 0;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) a.V[X.at(f, i, j, k)] = v[f];
+  }
+  if (floors) atomicAdd(a.counters + 0, (unsigned long long)floors);
+  if (bad != ULLONG_MAX) atomicMin(a.bad + a.stage, bad);
+}
+
+// 3-4: face i-1/2 (along D) of every cell: reconstruction, staggered normal field, face solve
+template <int D, int RS, int REC>
+__global__ void __launch_bounds__(128) k_ct_face(CtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  constexpr int oi = D == 0, oj = D == 1, ok = D == 2;
+  int fbs = 0, hlls = 0;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    double c[6][8];  // cells -3..+2 relative to cell (i,j,k) along D (PLM uses -2..+1)
+    constexpr int lo = REC == 2 ? -3 : -2, hi = REC == 2 ? 2 : 1;
+#pragma unroll
+    for (int s = lo; s <= hi; ++s)
+#pragma unroll
+      for (int f = 0; f < 8; ++f) c[s + 3][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
+    double vl[8], vr[8], tmp[8];
+    bool fb;
+    if constexpr (REC == 2) {
+      weno_side<8, true>(c[0], c[1], c[2], c[3], c[4], vl);        // left cell: q+
+      fb = weno_side<8, false>(c[1], c[2], c[3], c[4], c[5], vr);  // right cell: q-
+    } else {
+      plm_cell<8, REC>(c[1], c[2], c[3], vl, tmp);
+      fb = plm_cell<8, REC>(c[2], c[3], c[4], tmp, vr);
+    }
+    fbs += fb ? 1 : 0;
+    const double b = __ldg(a.Uin + X.at(5 + D, i, j, k));  // the staggered normal field of this face
+    vl[5 + D] = b;
+    vr[5 + D] = b;
+    double wl[8], wr[8], fn[8], fx[8];
+    to_normal<8, D>(vl, wl);
+    to_normal<8, D>(vr, wr);
+    hlls += face_flux<8, RS>(wl, wr, a.c, fn);
+    from_normal<8, D>(fn, fx);
+    double* F = a.F[D];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) F[X.at(f, i, j, k)] = fx[f];
+  }
+  if (fbs) atomicAdd(a.counters + 1, (unsigned long long)fbs);
+  if (hlls) atomicAdd(a.counters + 2, (unsigned long long)hlls);
+}
+
+// edge EMFs (arithmetic average of the four adjacent face EMFs, R32)
+__device__ __forceinline__ double ct_ez(const CtArgs& a, const CtIdx& X, int i, int j, int k) {  // edge (i-1/2, j-1/2)
+  const double e0 = -a.F[0][X.at(6, i, j - 1, k)], e1 = -a.F[0][X.at(6, i, j, k)];
+  const double e2 = a.F[1][X.at(5, i - 1, j, k)], e3 = a.F[1][X.at(5, i, j, k)];
+  return 0.25 * (((e0 + e1) + e2) + e3);
+}
+__device__ __forceinline__ double ct_ex(const CtArgs& a, const CtIdx& X, int i, int j, int k) {  // edge (j-1/2, k-1/2)
+  const double e0 = -a.F[1][X.at(7, i, j, k - 1)], e1 = -a.F[1][X.at(7, i, j, k)];
+  const double e2 = a.F[2][X.at(6, i, j - 1, k)], e3 = a.F[2][X.at(6, i, j, k)];
+  return 0.25 * (((e0 + e1) + e2) + e3);
+}
+__device__ __forceinline__ double ct_ey(const CtArgs& a, const CtIdx& X, int i, int j, int k) {  // edge (i-1/2, k-1/2)
+  const double e0 = -a.F[2][X.at(5, i - 1, j, k)], e1 = -a.F[2][X.at(5, i, j, k)];
+  const double e2 = a.F[0][X.at(7, i, j, k - 1)], e3 = a.F[0][X.at(7, i, j, k)];
+  return 0.25 * (((e0 + e1) + e2) + e3);
+}
+
+// 5-6 + RK epilogue
+__global__ void __launch_bounds__(256) k_ct_update(CtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  const double* lam = a.c.lam;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    double s[8];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      double r = lam[0] * (a.F[0][X.at(f, i + 1, j, k)] - a.F[0][X.at(f, i, j, k)]);
+      r = r + lam[1] * (a.F[1][X.at(f, i, j + 1, k)] - a.F[1][X.at(f, i, j, k)]);
+      r = r + lam[2] * (a.F[2][X.at(f, i, j, k + 1)] - a.F[2][X.at(f, i, j, k)]);
+      s[f] = __ldg(a.Uin + X.at(f, i, j, k)) - r;
+    }
+    const double ez = ct_ez(a, X, i, j, k), ex = ct_ex(a, X, i, j, k), ey = ct_ey(a, X, i, j, k);
+    const double rbx = lam[1] * (ct_ez(a, X, i, j + 1, k) - ez) - lam[2] * (ct_ey(a, X, i, j, k + 1) - ey);
+    const double rby = lam[2] * (ct_ex(a, X, i, j, k + 1) - ex) - lam[0] * (ct_ez(a, X, i + 1, j, k) - ez);
+    const double rbz = lam[0] * (ct_ey(a, X, i + 1, j, k) - ey) - lam[1] * (ct_ex(a, X, i, j + 1, k) - ex);
+    s[5] = __ldg(a.Uin + X.at(5, i, j, k)) - rbx;
+    s[6] = __ldg(a.Uin + X.at(6, i, j, k)) - rby;
+    s[7] = __ldg(a.Uin + X.at(7, i, j, k)) - rbz;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const size_t o = X.at(f, i, j, k);
+      double v = s[f];
+      if (a.mode == 1) v = 0.5 * (a.Un[o] + s[f]);
+      else if (a.mode == 2) v = (a.wa * a.Un[o]) + (a.wb * s[f]);
+      a.Uout[o] = v;
+    }
+  }
+}
+
+template <int RS, int REC>
+static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st) {
+  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  const unsigned g256 = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 16);
+  const unsigned g128 = (unsigned)std::min<size_t>((n + 127) / 128, (size_t)nsm * 32);
+  k_ct_prim<<<g256, 256, 0, st>>>(a);
+  k_ct_face<0, RS, REC><<<g128, 128, 0, st>>>(a);
+  k_ct_face<1, RS, REC><<<g128, 128, 0, st>>>(a);
+  k_ct_face<2, RS, REC><<<g128, 128, 0, st>>>(a);
+  k_ct_update<<<g256, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st) {
+  const int lim = a.c.limiter;
+  if (riemann) {
+    if (lim == 2) return launch_ct_t<1, 2>(a, nsm, st);
+    if (lim == 1) return launch_ct_t<1, 1>(a, nsm, st);
+    return launch_ct_t<1, 0>(a, nsm, st);
+  }
+  if (lim == 2) return launch_ct_t<0, 2>(a, nsm, st);
+  if (lim == 1) return launch_ct_t<0, 1>(a, nsm, st);
+  return launch_ct_t<0, 0>(a, nsm, st);
+}
+
+// dt / c_h maxima with the face-averaged B (3.12 with R32)
+__global__ void __launch_bounds__(256) k_ct_dt(DtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz_loc, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const size_t n = (size_t)a.nx * a.ny * a.nz_loc;
+  double M = 0.0, Sx = 0.0;
+  unsigned long long bad = ULLONG_MAX;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    double u[8], v[8];
+    ct_cell_cons(a.U, X, i, j, k, u);
+    if (bad_state<8>(u)) {
+      bad = min(bad, (unsigned long long)q);
+      continue;
+    }
+    cons2prim<8>(u, v, a.gm1, a.p_floor);
+    double inv = 0.0, smax = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double cf = fast_speed(a.gamma, v[0], v[4], v[5 + d], v[5 + (d + 1) % 3], v[5 + (d + 2) % 3]);
+      const double s = fabs(v[1 + d]) + cf;
+      if (d == 0) {
+        inv = s * a.idx[0];
+        smax = s;
+      } else {
+        inv = inv + s * a.idx[d];
+        smax = fmax(smax, s);
+      }
+    }
+    M = fmax(M, inv);
+    Sx = fmax(Sx, smax);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    Sx = fmax(Sx, __shfl_xor_sync(0xffffffffu, Sx, o));
+  }
+  __shared__ double red[2][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][w] = M;
+    red[1][w] = Sx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int r = 1; r < (int)(blockDim.x >> 5); ++r) {
+      M = fmax(M, red[0][r]);
+      Sx = fmax(Sx, red[1][r]);
+    }
+    atomicMax(a.out + 0, (unsigned long long)__double_as_longlong(M));
+    atomicMax(a.out + 1, (unsigned long long)__double_as_longlong(Sx));
+  }
+  if (bad != ULLONG_MAX) atomicMin(a.bad, bad);
+}
+
+cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st) {
+  const size_t n = (size_t)a.nx * a.ny * a.nz_loc;
+  const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 8);
+  k_ct_dt<<<g > 0 ? g : 1, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace mhd

@@ -493,7 +493,7 @@ __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst,
 // set_state validation: rho > 0, p > 0 (before any floor), all finite
 template <int NV>
 __global__ void k_validate(const double* __restrict__ U, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
-                           unsigned long long* bad) {
+                           unsigned long long* bad, int check_p) {
   const size_t fstride = (size_t)nx * ny, pstride = fstride * NV, ncell = fstride * nzl;
   unsigned long long b = ULLONG_MAX;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ncell; i += (size_t)gridDim.x * blockDim.x) {
@@ -501,7 +501,7 @@ __global__ void k_validate(const double* __restrict__ U, int nx, int ny, int nzl
     double u[NV], v[NV];
     load_cell<NV>(U, (k + gz) * pstride, fstride, cell, u);
     bool bad = bad_state<NV>(u);
-    if (!bad) {
+    if (!bad && check_p) {
       cons2prim<NV>(u, v, gm1, -1.0e300);
       bad = !(v[4] > 0.0);
     }
@@ -631,9 +631,9 @@ cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, 
 }
 
 cudaError_t launch_validate(const double* U, int nv, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
-                            unsigned long long* bad, int nsm, cudaStream_t st) {
-  if (nv == 9) k_validate<9><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad);
-  else k_validate<8><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad);
+                            unsigned long long* bad, int nsm, cudaStream_t st, int check_p) {
+  if (nv == 9) k_validate<9><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad, check_p);
+  else k_validate<8><<<nsm * 8, 256, 0, st>>>(U, nx, ny, nzl, gz, zoff, gm1, bad, check_p);
   return cudaGetLastError();
 }
 

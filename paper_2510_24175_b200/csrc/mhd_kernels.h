@@ -41,13 +41,30 @@ struct DtArgs {
 };
 
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st);
+
+// constrained transport (mhd_ct.cu): 3D, periodic, one GPU, 8 fields (b on faces)
+struct CtArgs {
+  const double* Uin;  // stage input (padded [z+gz][8][y][x], ghost planes unused: periodic wrap)
+  const double* Un;   // U^n for the RK epilogue
+  double* Uout;
+  double* V;          // scratch: cell-centred primitives
+  double* F[3];       // scratch: face fluxes per direction (induction entries = face EMFs)
+  int nx, ny, nz, gz;
+  int stage, mode, last;
+  double wa, wb;
+  StageConsts c;
+  unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
+  unsigned long long* bad;       // [4] per stage
+};
+cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st);
+cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st);
 int stage_tile_rows(int dim, int limiter);
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter);  // resident CTAs per SM of the stage kernel
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st);
 cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, int nzl, int gz, int to_internal,
                         int nsm, cudaStream_t st);
 cudaError_t launch_validate(const double* U, int nv, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
-                            unsigned long long* bad, int nsm, cudaStream_t st);
+                            unsigned long long* bad, int nsm, cudaStream_t st, int check_p);
 cudaError_t launch_face_flux(int nv, int riemann, const double* VL, const double* VR, long long n,
                              const StageConsts& c, double* F, unsigned long long* nhll, cudaStream_t st);
 

@@ -42,7 +42,7 @@ class BC(C.Structure):
 
 class Scheme(C.Structure):
     _fields_ = [("limiter", C.c_int32), ("riemann", C.c_int32), ("glm", C.c_int32), ("stepper", C.c_int32),
-                ("glm_alpha", C.c_double), ("p_floor", C.c_double)]
+                ("glm_alpha", C.c_double), ("p_floor", C.c_double), ("ct", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Dist(C.Structure):
@@ -155,7 +155,7 @@ class Solver:
             bc.lo[d] = int(problem.bc[d])
             bc.hi[d] = int(problem.bc[d])
         sc = Scheme(int(problem.limiter), int(problem.riemann), int(problem.glm), int(getattr(problem, "stepper", 0)),
-                    float(problem.glm_alpha), float(problem.p_floor))
+                    float(problem.glm_alpha), float(problem.p_floor), int(getattr(problem, "ct", 0)), 0)
         dist = None
         if nranks > 1 or device >= 0:
             dist = Dist(rank, nranks, device, transport)

@@ -64,7 +64,9 @@ def test_create_rejects_bad_arguments_without_gpu(lib):
     g.hi[1] = 0.0
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), None, None, C.byref(h)) == mhd.MHD_E_ARG
     g.hi[1] = 1.0
-    sc = mhd.Scheme(1, 1, 0, 0, 0.1, 1e-12)  # no GLM in 3D
+    sc = mhd.Scheme(1, 1, 0, 0, 0.1, 1e-12, 0, 0)  # no GLM in 3D
+    assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), C.byref(sc), None, C.byref(h)) == mhd.MHD_E_ARG
+    sc = mhd.Scheme(1, 1, 1, 0, 0.1, 1e-12, 1, 0)  # CT together with GLM
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), C.byref(sc), None, C.byref(h)) == mhd.MHD_E_ARG
     d = mhd.Dist(0, 3, -1, 0)                # 3 ranks do not divide nz = 16
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), None, C.byref(d), C.byref(h)) == mhd.MHD_E_ARG

@@ -396,3 +396,30 @@ def test_wenoz_slab_group_bitwise(mhd):
     U4 = g.get_state()
     g.destroy()
     assert np.array_equal(log1, log4) and np.array_equal(U1, U4)
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) row 4: constrained transport (face-centred b, edge EMFs), 3D periodic
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["cpa_mc_rk2", "ot_hll", "random_wenoz_rk3", "ragged_minmod"])
+def test_ct_parity(mhd, case):
+    from test_oracle_scheme import _random_ct_state
+    if case == "cpa_mc_rk2":
+        p = I.ct_problem(I.cpa_3d(16))
+        U0 = I.cpa_3d_ct_ic(p)
+        n = 40
+    elif case == "ot_hll":
+        p = I.ct_problem(I.orszag_tang_3d(24, riemann=I.HLL))
+        U0 = I.orszag_tang_3d_ic(p.replace(ct=0, glm=1))[:8].copy()
+        n = 12
+    elif case == "random_wenoz_rk3":
+        p = I.orszag_tang_3d(12, limiter=I.WENOZ).replace(ct=1, glm=0, stepper=I.RK3)
+        U0 = _random_ct_state(p)
+        n = 10
+    else:
+        p = I.orszag_tang_3d(12, limiter=I.MINMOD).replace(n=(37, 14, 9), ct=1, glm=0)
+        U0 = _random_ct_state(p)
+        n = 10
+    res = run_both(mhd, p, U0, n)
+    assert_parity(*res)
+    assert np.abs(oracle.ct_divb(p, res[2])).max() < 1e-10
