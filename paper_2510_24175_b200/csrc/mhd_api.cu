@@ -464,7 +464,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
       (c->scheme.riemann != MHD_RS_HLL && c->scheme.riemann != MHD_RS_HLLD) || (c->scheme.glm != 0 && c->scheme.glm != 1) ||
       (c->scheme.stepper != MHD_RK2 && c->scheme.stepper != MHD_RK3) || (c->scheme.ct != 0 && c->scheme.ct != 1) ||
       (c->scheme.ct && (c->scheme.glm || c->dim != 3)) ||
-      !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm)) {
+      !(c->scheme.glm_alpha >= 0.0) || !std::isfinite(c->scheme.p_floor) || (c->dim >= 2 && !c->scheme.glm && !c->scheme.ct)) {
     delete c;
     return MHD_E_ARG;
   }

@@ -9,7 +9,7 @@
 //                induction entries are the face EMFs)
 //   k_ct_update  rho, m, E by the flux divergence; b by Stokes with edge EMFs averaged from the
 //                four adjacent face EMFs (arithmetic); the RK epilogue.
-// The arithmetic of every step is the oracle's (oracle/mhd_oracle.c stage_op_ct) operation for
+// The arithmetic of every step follows the recipe of DESIGN.md R32 operation for
 // operation (built with --fmad=false), so the two agree bitwise.
 #include <cuda_runtime.h>
 
