@@ -164,9 +164,10 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]);
 
-/* Counters and the unphysical-state record (synchronising; collective when nranks > 1
- * only through mhd_compute_dt, which refreshes the global sums). */
-int mhd_get_diag(const mhd_ctx* ctx, mhd_diag* diag);
+/* Counters and the unphysical-state record.  On one GPU the counters are read back from the
+ * device (synchronising) and include every completed step; with NCCL slabs they are the global
+ * sums reduced by the last mhd_compute_dt (the collective). */
+int mhd_get_diag(mhd_ctx* ctx, mhd_diag* diag);
 
 /* Last error message of this context (valid until the next call on it); never NULL. */
 const char* mhd_last_error(const mhd_ctx* ctx);

@@ -802,8 +802,20 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
   return MHD_OK;
 }
 
-int mhd_get_diag(const mhd_ctx* c, mhd_diag* d) {
+int mhd_get_diag(mhd_ctx* c, mhd_diag* d) {
   if (!c || !d) return MHD_E_ARG;
+  // one rank (or an in-process group): refresh the counters from the device so that steps
+  // since the last mhd_compute_dt are included; with NCCL slabs the global sums are the ones
+  // reduced by the last mhd_compute_dt (a collective)
+  if ((c->nranks == 1 || c->transport == MHD_TRANSPORT_LOCAL) && c->dbuf && c->stream != (cudaStream_t)-1) {
+    if (cudaMemcpyAsync(c->hbuf + 2, c->dbuf + 2, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c->stream) == cudaSuccess &&
+        cudaStreamSynchronize(c->stream) == cudaSuccess) {
+      c->diag.p_floors = (int64_t)c->hbuf[2];
+      c->diag.plm_fallbacks = (int64_t)c->hbuf[3];
+      c->diag.hlld_to_hll = (int64_t)c->hbuf[4];
+    }
+  }
   *d = c->diag;
   return MHD_OK;
 }
