@@ -45,6 +45,9 @@ _WZ = 19 + 3 * 1278 + 3 * 243 + 81
 FLOPS_PER_LAUNCH_AVG = {"plm-rk2": (FLOPS_CELL_STAGE[1] + FLOPS_CELL_STAGE[2]) / 2.0,
                         "wenoz-rk3": (_WZ + (_WZ + 27) + (_WZ + 28)) / 3.0}
 BYTES_PER_LAUNCH_AVG = {"plm-rk2": (2 * NV * 8 + 3 * NV * 8) / 2.0, "wenoz-rk3": (2 * NV * 8 + 3 * NV * 8 * 2) / 3.0}
+# CT stages are five launches (prim, 3 face passes, update); their roofline is not the fused kernel's
+FLOPS_PER_LAUNCH_AVG.update({"ct-plm-rk2": None, "ct-wenoz-rk3": None})
+BYTES_PER_LAUNCH_AVG.update({"ct-plm-rk2": None, "ct-wenoz-rk3": None})
 N_SM, FP64_LANES_PER_SM = 148, 64
 
 
@@ -106,6 +109,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
+SCHEMES = {
+    "plm-rk2": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4",
+    "wenoz-rk3": "WENOZ + HLLD + GLM, SSP-RK3, CFL 0.4",
+    "ct-plm-rk2": "PLM-MC + HLLD + constrained transport, SSP-RK2, CFL 0.4",
+    "ct-wenoz-rk3": "WENOZ + HLLD + constrained transport, SSP-RK3, CFL 0.4",
+}
 WORKLOADS = {
     "ot3d": "3D Orszag-Tang (BASELINE configs[2] at 256^3, configs[4] at 1024^3)",
     "blast3d": "3D MHD blast, one blast per GPU cube (BASELINE configs[3], 512^3 per GPU)",
@@ -124,8 +133,10 @@ def build_problem(workload: str, n_gpus: int, n: int, scheme: str = "plm-rk2"):
         p = I.cpa_3d(n).replace(n=(n, n, n * n_gpus), hi=(1.0, 1.0, float(n_gpus)))
     else:
         raise ValueError(workload)
-    if scheme == "wenoz-rk3":
+    if scheme.endswith("wenoz-rk3"):
         p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    if scheme.startswith("ct-"):
+        p = I.ct_problem(p)
     return p
 
 
@@ -133,11 +144,15 @@ def build_ic(workload: str, p, z0: int, z1: int, chunk: int = 64):
     """initial condition of global planes [z0, z1), generated in z chunks into one array (keeps
     the host peak near the array size for 1024^3)"""
     from paper_2510_24175_b200 import inputs as I
+    if p.ct and workload == "cpa3d":  # face fields from the edge vector potential (whole grid)
+        assert (z0, z1) == (0, p.n[2])
+        return I.cpa_3d_ct_ic(p)
     fn = {"ot3d": I.orszag_tang_3d_ic, "blast3d": I.blast_3d_ic, "cpa3d": I.cpa_3d_ic}[workload]
+    pg = p.replace(ct=0, glm=1) if p.ct else p  # OT and blast fields are face-exact: CT takes fields 0..7
     U = np.empty((p.nvar, z1 - z0, p.n[1], p.n[0]), dtype=np.float64)
     for a in range(z0, z1, chunk):
         b = min(z1, a + chunk)
-        U[:, a - z0:b - z0] = fn(p, z_range=(a, b))
+        U[:, a - z0:b - z0] = fn(pg, z_range=(a, b))[:p.nvar]
     return U
 
 
@@ -198,9 +213,10 @@ def main():
     ap.add_argument("--impl", default="mhd", choices=["mhd", "reference"])
     ap.add_argument("--n", type=int, default=256, help="cells per axis per GPU (configs[2]: 256)")
     ap.add_argument("--workload", default="ot3d", choices=sorted(WORKLOADS))
-    ap.add_argument("--scheme", default="plm-rk2", choices=["plm-rk2", "wenoz-rk3"],
+    ap.add_argument("--scheme", default="plm-rk2", choices=sorted(SCHEMES),
                     help="plm-rk2: the north star's PLM-MC + HLLD + GLM + SSP-RK2 (default); wenoz-rk3: the "
-                         "paper's WENOZ + HLLD + GLM + SSP-RK3 (PAPER.md:179, 270)")
+                         "paper's strong-scaling WENOZ + HLLD + GLM + SSP-RK3 (PAPER.md:270); ct-wenoz-rk3: its "
+                         "weak-scaling WENOZ + HLLD + CT + SSP-RK3 (PAPER.md:179, one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=256, help="cpu_baseline sample: planes of the grid")
@@ -280,8 +296,9 @@ def main():
     dt_ms, dt_n = prof["dt"]
     cells_loc = p.cells // world
     stage_avg_s = stage_ms * 1e-3 / max(stage_n, 1)
-    flops_launch = cells_loc * FLOPS_PER_LAUNCH_AVG[args.scheme]  # average over the step's stages
-    bytes_launch = cells_loc * BYTES_PER_LAUNCH_AVG[args.scheme]
+    ct = args.scheme.startswith("ct-")
+    flops_launch = cells_loc * (FLOPS_PER_LAUNCH_AVG[args.scheme] or FLOPS_PER_LAUNCH_AVG["plm-rk2"])
+    bytes_launch = cells_loc * (BYTES_PER_LAUNCH_AVG[args.scheme] or BYTES_PER_LAUNCH_AVG["plm-rk2"])
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     fp64_peak = N_SM * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12  # TFLOP/s, 1 op per lane per clock (no FMA)
     achieved = flops_launch / stage_avg_s / 1e12
@@ -304,6 +321,11 @@ def main():
             "ncu": (ncu or None) if args.scheme == "plm-rk2" else None}
     if args.scheme != "plm-rk2":
         roof["traffic"] = None
+    if ct:  # the timed unit is a 5-launch stage, not the fused kernel: report the stage time only
+        roof = {"bound": "alu", "achieved": None, "peak": fp64_peak, "unit": "TFLOP/s", "frac": None,
+                "traffic": None, "kernel": "CT stage (k_ct_prim + 3 x k_ct_face + k_ct_update)",
+                "stage_ms_per_launch": stage_avg_s * 1e3, "stage_launches": stage_n,
+                "stage_share_of_step": stage_ms / max(ms, 1e-9)}
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -342,10 +364,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{args.workload}_{args.n}^3_per_gpu ({WORKLOADS[args.workload]}; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
-                           "scheme": {"plm-rk2": "PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4",
-                                      "wenoz-rk3": "WENOZ + HLLD + GLM, SSP-RK3, CFL 0.4"}[args.scheme], "cells": cells,
+                           "scheme": SCHEMES[args.scheme], "cells": cells,
                            "parallelism": f"z-slab x{world}", "l2": "inputs larger than L2 (2 x 1.27 GB arrays per GPU)"},
-                "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * 3,
+                "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * (1 + (3 if p.stepper else 2) * (5 if p.ct else 1)),
                 "e2e": e2e, "cpu_baseline": cpu, "diag": diag,
                 "lib": mhd.version()}
         print(json.dumps(line), flush=True)
