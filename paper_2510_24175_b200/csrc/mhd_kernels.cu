@@ -72,7 +72,8 @@ struct StageSmem {
   static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vpz, Fz[0], Fz[1] each
   static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
   static constexpr int nFx = NV * TY * (TX + 1);
-  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx);
+  static constexpr int nXP = NV * TY;  // q+ (x) of cell x0-1 per row, from the edge warp (PLM)
+  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx + nXP);
 };
 
 #ifndef MHD_OCCW
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   double* Fz = Vpz + S::nCol;        // [2][NV][NC] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
   double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
   double* Fx = Fy + S::nFy;          // [NV][TY][TX+1] x-face fluxes of plane k
+  double* XP = Fx + S::nFx;          // [NV][TY] q+ along x of cell x0-1 of every row (PLM)
 
   const StageConsts& c = a.c;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -236,6 +238,25 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         if (full && a.mode != 0) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
       }
     }
+    if (!WZ && full && !cellw) {
+      // PLM x faces: the cell warps reconstruct each cell once along x and pass q+ to the next
+      // lane; the edge warp supplies q+ of the cells x0-1 (lane 0's left neighbours) and then
+      // releases the cell warps' x jobs (named barrier 1: producer arrive / consumer sync)
+      if (tx < TY) {
+        double qa[NV], qb[NV], qc[NV], qp[NV], qm[NV];
+#pragma unroll
+        for (int f = 0; f < NV; ++f) {
+          const double* base = Vc + (f * PH + tx + HY) * PW + G - 1;
+          qa[f] = base[-1];
+          qb[f] = base[0];
+          qc[f] = base[1];
+        }
+        plm_cell<NV, LIM>(qa, qb, qc, qp, qm);
+#pragma unroll
+        for (int f = 0; f < NV; ++f) XP[f * TY + tx] = qp[f];
+      }
+      asm volatile("bar.arrive 1, %0;" ::"r"(NT) : "memory");
+    }
 #pragma unroll kJobUnroll
     for (int job = 0; job <= 3; ++job) {
       // ---- select the face of this job (warp-uniform activity)
@@ -305,6 +326,23 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
           to_normal<NV, 2>(qm, wr);
 #pragma unroll
           for (int f = 0; f < NV; ++f) Vpz[f * NC + tid] = wp[f];
+        } else if (!WZ && job == 3) {
+          // x face tx-1/2 (cell warps): own cell reconstructed once, left state from lane tx-1
+          double qa[NV], qb[NV], qc[NV], qp[NV];
+#pragma unroll
+          for (int n = 0; n < NV; ++n) {
+            const double* base = Vc + (n * PH + row + HY) * PW + col + G;
+            qa[n] = base[-1];
+            qb[n] = base[0];
+            qc[n] = base[1];
+          }
+          fb = plm_cell<NV, LIM>(qa, qb, qc, qp, wr);
+          asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // XP written by the edge warp
+#pragma unroll
+          for (int n = 0; n < NV; ++n) {
+            const double nb = __shfl_up_sync(0xffffffffu, qp[n], 1);
+            wl[n] = (tx == 0) ? XP[n * TY + ty] : nb;
+          }
         } else {
           const int s = (d == 0) ? 1 : PW;
           double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
