@@ -193,6 +193,16 @@ int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
 /* Library build identity, e.g. "libmhd sm_100a fused-v1". */
 const char* mhd_version(void);
 
+/* Test-only, no context: the branch-free division / reciprocal / square-root sequences of the
+ * face solve (mhd_device.cuh; value-neutral) next to the IEEE operators, for
+ * n pairs (a[i], b[i]).  a, b: DEVICE [n]; out: DEVICE [n][8] = (fast 1/b, 1.0/b, fast a/b,
+ * a/b, fast sqrt(a), sqrt(a), fast |a|/b, |a|/b); ok: DEVICE [n] bit mask of the sequences
+ * whose range test passed (bit 0 reciprocal, 1 division, 2 square root, 3 |a|/b — the last
+ * defined for positive normal b only) — where a bit is set the fast value must equal the
+ * IEEE one bitwise.  Runs on the current device's default stream and
+ * synchronises.  MHD_E_ARG on NULL pointers or n < 0, MHD_E_CUDA on a launch error. */
+int mhd_debug_fast_ops(const double* a, const double* b, int64_t n, double* out, int32_t* ok);
+
 #ifdef __cplusplus
 }
 #endif

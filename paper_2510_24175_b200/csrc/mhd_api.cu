@@ -879,4 +879,11 @@ int mhd_debug_face_flux(mhd_ctx* c, const double* VL, const double* VR, int64_t 
   return MHD_OK;
 }
 
+int mhd_debug_fast_ops(const double* a, const double* b, int64_t n, double* out, int32_t* ok) {
+  if (!a || !b || !out || !ok || n < 0) return MHD_E_ARG;
+  if (n == 0) return MHD_OK;
+  if (mhd::launch_fast_ops(a, b, n, out, ok, 0) != cudaSuccess) return MHD_E_CUDA;
+  return cudaDeviceSynchronize() == cudaSuccess ? MHD_OK : MHD_E_CUDA;
+}
+
 }  // extern "C"

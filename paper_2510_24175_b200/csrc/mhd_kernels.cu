@@ -52,6 +52,116 @@ __device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("pre
 __device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // ---------------------------------------------------------------------------------------
+// face-state gathers (shared by the marching path and the exact re-solve below)
+// ---------------------------------------------------------------------------------------
+// The two states of an x (d = 0) or y (d = 1) face from the primitive plane Vc [NV][PH][PW]:
+// face col-1/2 (x) or row-1/2 (y) of the tile cell (row, col); returns the right cell's
+// positivity fallback.  Vc is read with the frame permutation folded into the field addresses
+// (component n of the normal frame of direction d is field fo[n]); the reconstruction is
+// component-wise, so reconstructing in the normal frame is value-identical.
+template <int NV, int REC, int PH, int PW, int HY, int G>
+__device__ __forceinline__ bool gather_xy(const double* Vc, int d, int row, int col, double* wl, double* wr) {
+  constexpr int LIM = REC == 0 ? 0 : 1;
+  const int s = (d == 0) ? 1 : PW;
+  int fo[NV];
+#pragma unroll
+  for (int n = 0; n < NV; ++n) fo[n] = n;
+  if (d == 1) {
+    fo[1] = 2; fo[2] = 3; fo[3] = 1; fo[5] = 6; fo[6] = 7; fo[7] = 5;
+  }
+  double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
+  if constexpr (REC == 2) {  // WENO-Z: left cell from v[-3..1], right cell from v[-2..2]
+    double qaa[NV], qdd[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) {
+      const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
+      qaa[n] = base[-3 * s];
+      qa[n] = base[-2 * s];
+      qb[n] = base[-s];
+      qc[n] = base[0];
+      qd[n] = base[s];
+      qdd[n] = base[2 * s];
+    }
+    weno_side<NV, true>(qaa, qa, qb, qc, qd, wl);        // left cell: V+
+    return weno_side<NV, false>(qa, qb, qc, qd, qdd, wr);  // right cell: V-
+  } else {
+#pragma unroll
+    for (int n = 0; n < NV; ++n) {
+      const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
+      qa[n] = base[-2 * s];
+      qb[n] = base[-s];
+      qc[n] = base[0];
+      qd[n] = base[s];
+    }
+    plm_cell<NV, LIM>(qa, qb, qc, wl, tmp);       // left cell: V+
+    return plm_cell<NV, LIM>(qb, qc, qd, tmp, wr);  // right cell: V-
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void convert_at(const double* __restrict__ Ucol, size_t fstride, double gm1, double pf,
+                                           double* v) {
+  double u[NV];
+#pragma unroll
+  for (int f = 0; f < NV; ++f) u[f] = __ldg(Ucol + f * fstride);
+  cons2prim<NV>(u, v, gm1, pf);
+}
+
+// The two states of the z face k+1/2 of one column straight from the conservative planes
+// (Ucol: the column's cell in storage plane 0): the same conversions and reconstructions as
+// the marching path, which carries V+(k) in shared memory instead.
+template <int NV, int REC>
+__device__ __forceinline__ void gather_z(const double* __restrict__ Ucol, size_t pstride, size_t fstride, int k,
+                                         double gm1, double pf, double* wl, double* wr) {
+  constexpr int LIM = REC == 0 ? 0 : 1;
+  double qp[NV], qm[NV];
+  auto at = [&](int kk) { return Ucol + (ptrdiff_t)kk * (ptrdiff_t)pstride; };
+  if constexpr (REC == 2) {
+    double q0[NV], q1[NV], q2[NV], q3[NV], q4[NV];
+    convert_at<NV>(at(k - 2), fstride, gm1, pf, q0);
+    convert_at<NV>(at(k - 1), fstride, gm1, pf, q1);
+    convert_at<NV>(at(k), fstride, gm1, pf, q2);
+    convert_at<NV>(at(k + 1), fstride, gm1, pf, q3);
+    convert_at<NV>(at(k + 2), fstride, gm1, pf, q4);
+    weno_cell<NV>(q0, q1, q2, q3, q4, qp, qm);
+    to_normal<NV, 2>(qp, wl);
+    convert_at<NV>(at(k + 3), fstride, gm1, pf, q0);
+    weno_cell<NV>(q1, q2, q3, q4, q0, qp, qm);
+    to_normal<NV, 2>(qm, wr);
+  } else {
+    double q0[NV], q1[NV], q2[NV];
+    convert_at<NV>(at(k - 1), fstride, gm1, pf, q0);
+    convert_at<NV>(at(k), fstride, gm1, pf, q1);
+    convert_at<NV>(at(k + 1), fstride, gm1, pf, q2);
+    plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
+    to_normal<NV, 2>(qp, wl);
+    convert_at<NV>(at(k + 2), fstride, gm1, pf, q0);
+    plm_cell<NV, LIM>(q1, q2, q0, qp, qm);
+    to_normal<NV, 2>(qm, wr);
+  }
+}
+
+// The face solve with the plain IEEE operators, its states re-derived: taken only when a
+// range test of the branch-free operators failed (mhd_device.cuh).  Out of line so that the
+// marching path keeps neither the inputs of its solve nor a second solve in its registers.
+template <int NV>
+struct FaceOut {
+  double f[NV];
+  int fell;
+};
+template <int NV, int RS, int REC, int PH, int PW, int HY, int G>
+__device__ __noinline__ FaceOut<NV> exact_face(StageConsts c, const double* Vc, const double* Ucol, size_t pstride,
+                                               size_t fstride, int kplane, int d, int row, int col) {
+  double vl[NV], vr[NV];
+  if (d == 2) gather_z<NV, REC>(Ucol, pstride, fstride, kplane, c.gm1, c.p_floor, vl, vr);
+  else gather_xy<NV, REC, PH, PW, HY, G>(Vc, d, row, col, vl, vr);
+  FaceOut<NV> o;
+  bool unused = true;
+  o.fell = face_flux_t<NV, RS, false>(vl, vr, c, o.f, unused);
+  return o;
+}
+
+// ---------------------------------------------------------------------------------------
 // fused stage kernel
 #ifndef MHD_JOB_UNROLL
 #define MHD_JOB_UNROLL 1
@@ -290,16 +400,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         cnt_face = own || (gx == nx && gy < ny);
       }
       if (!active) continue;
-      // ---- gather the two face states (normal frame) with PLM
-      // x/y jobs read Vc with the frame permutation folded into the field addresses
-      // (component n of the normal frame of direction d is field fo[n]); PLM is
-      // component-wise, so reconstructing in the normal frame is value-identical.
-      int fo[NV];
-#pragma unroll
-      for (int n = 0; n < NV; ++n) fo[n] = n;
-      if (d == 1) {
-        fo[1] = 2; fo[2] = 3; fo[3] = 1; fo[5] = 6; fo[6] = 7; fo[7] = 5;
-      }
+      // ---- gather the two face states (normal frame)
       double wl[NV], wr[NV];
       {
         bool fb;
@@ -344,40 +445,23 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             wl[n] = (tx == 0) ? XP[n * TY + ty] : nb;
           }
         } else {
-          const int s = (d == 0) ? 1 : PW;
-          double qa[NV], qb[NV], qc[NV], qd[NV], tmp[NV];
-          if constexpr (WZ) {  // left cell from v[-3..1], right cell from v[-2..2]
-            double qaa[NV], qdd[NV];
-#pragma unroll
-            for (int n = 0; n < NV; ++n) {
-              const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
-              qaa[n] = base[-3 * s];
-              qa[n] = base[-2 * s];
-              qb[n] = base[-s];
-              qc[n] = base[0];
-              qd[n] = base[s];
-              qdd[n] = base[2 * s];
-            }
-            weno_side<NV, true>(qaa, qa, qb, qc, qd, wl);        // left cell: V+
-            fb = weno_side<NV, false>(qa, qb, qc, qd, qdd, wr);  // right cell: V-
-          } else {
-#pragma unroll
-            for (int n = 0; n < NV; ++n) {
-              const double* base = Vc + (fo[n] * PH + row + HY) * PW + col + G;
-              qa[n] = base[-2 * s];
-              qb[n] = base[-s];
-              qc[n] = base[0];
-              qd[n] = base[s];
-            }
-            plm_cell<NV, LIM>(qa, qb, qc, wl, tmp);       // left cell: V+
-            fb = plm_cell<NV, LIM>(qb, qc, qd, tmp, wr);  // right cell: V-
-          }
+          fb = gather_xy<NV, REC, PH, PW, HY, G>(Vc, d, row, col, wl, wr);
         }
         if (fb && cnt_right) atomicAdd(&s_cnt[1], 1);
       }
-      // ---- the face solve (single instance)
+      // ---- the face solve (single instance, branch-free division / square root)
       double fn[NV];
-      const int fell = face_flux<NV, RS>(wl, wr, c, fn);
+      bool ok = true;
+      int fell = face_flux_t<NV, RS, true>(wl, wr, c, fn, ok);
+      if (!ok) {
+        // a range test of the branch-free operators failed (rare): the plain operators on the
+        // same face, its two states re-derived from shared memory (x, y) or the planes (z)
+        const FaceOut<NV> o = exact_face<NV, RS, REC, PH, PW, HY, G>(c, Vc, a.Uin + own_cell + (size_t)a.gz * pstride,
+                                                                     pstride, fstride, k, d, row, col);
+#pragma unroll
+        for (int f = 0; f < NV; ++f) fn[f] = o.f[f];
+        fell = o.fell;
+      }
       if (fell && cnt_face) atomicAdd(&s_cnt[2], 1);
       // ---- scatter (back to x,y,z components through the same field map)
       if (job == 0) {
@@ -402,19 +486,18 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       __syncthreads();
       continue;
     }
-    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads are
-    // issued before the barrier so their latency overlaps the wait.
+    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads of U
+    // and U^n follow the barrier (held across it they would spill; both planes were prefetched
+    // into L1 at the top of the iteration).
     const size_t off = plane_off(k) + (size_t)gy * nx + gx;
-    double u0[NV], un[NV];
+    __syncthreads();
     if (own) {
+      double u0[NV], un[NV];
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
         u0[f] = __ldg(a.Uin + off + f * fstride);
         un[f] = (a.mode != 0) ? a.Un[off + f * fstride] : 0.0;
       }
-    }
-    __syncthreads();
-    if (own) {
       const double* fzn = Fz + ((k + 1) & 1) * S::nCol;
       const double* fzo = Fz + (k & 1) * S::nCol;
 #pragma unroll
@@ -565,6 +648,30 @@ __global__ void k_face_flux(const double* __restrict__ VL, const double* __restr
     for (int f = 0; f < NV; ++f) F[q * NV + f] = fn[f];
   }
   if (cnt) atomicAdd(nhll, (unsigned long long)cnt);
+}
+
+// test-only: the branch-free operator sequences next to the IEEE operators (mhd_device.cuh)
+__global__ void k_fast_ops(const double* __restrict__ A, const double* __restrict__ B, long long n,
+                           double* __restrict__ out, int* __restrict__ okm) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const double a = A[q], b = B[q];
+    bool o0 = true, o1 = true, o2 = true, o3 = true;
+    out[q * 8 + 0] = fast_rcp(b, o0);
+    out[q * 8 + 1] = 1.0 / b;
+    out[q * 8 + 2] = fast_div(a, b, div_rcp(b), o1);
+    out[q * 8 + 3] = a / b;
+    out[q * 8 + 4] = fast_sqrt(a, o2);
+    out[q * 8 + 5] = sqrt(a);
+    out[q * 8 + 6] = fast_div_b(fabs(a), b, o3);
+    out[q * 8 + 7] = fabs(a) / b;
+    okm[q] = (int)o0 | ((int)o1 << 1) | ((int)o2 << 2) | ((int)o3 << 3);
+  }
+}
+
+cudaError_t launch_fast_ops(const double* A, const double* B, long long n, double* out, int* okm, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1);
+  k_fast_ops<<<blocks < 4096u ? blocks : 4096u, 256, 0, st>>>(A, B, n, out, okm);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------

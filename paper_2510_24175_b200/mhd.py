@@ -28,7 +28,7 @@ _NAMES = {0: "MHD_OK", 1: "MHD_E_ARG", 2: "MHD_E_STATE", 3: "MHD_E_CUDA", 4: "MH
 EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_box", "mhd_device_bytes",
            "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
-           "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan")
+           "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -94,6 +94,8 @@ def load() -> C.CDLL:
     L.mhd_destroy.restype = None
     L.mhd_debug_face_flux.argtypes = [P, P, P, C.c_int64, C.c_double, P, C.POINTER(C.c_int64)]
     L.mhd_version.restype = C.c_char_p
+    if hasattr(L, "mhd_debug_fast_ops"):  # (absent from older builds used in A/B runs)
+        L.mhd_debug_fast_ops.argtypes = [P, P, C.c_int64, P, P]
     L.mhd_profile_enable.argtypes = [P, C.c_int32]
     L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.mhd_group_compute_dt.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(C.c_double)]
@@ -123,6 +125,19 @@ def halo_plan(rank: int, nranks: int, nz_glob: int, z_periodic: bool = True, gho
     if rc:
         raise MhdError(rc, "mhd_halo_plan")
     return [tuple(buf[4 * i:4 * i + 4]) for i in range(4)]
+
+
+def debug_fast_ops(a, b):
+    """Test-only: (out [n][8], ok [n]) of mhd_debug_fast_ops for CUDA float64 tensors a, b."""
+    import torch
+    L = load()
+    out = torch.empty((a.shape[0], 8), dtype=torch.float64, device=a.device)
+    ok = torch.empty(a.shape[0], dtype=torch.int32, device=a.device)
+    rc = L.mhd_debug_fast_ops(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), a.shape[0],
+                              C.c_void_p(out.data_ptr()), C.c_void_p(ok.data_ptr()))
+    if rc != 0:
+        raise MhdError(rc, "mhd_debug_fast_ops failed")
+    return out, ok
 
 
 def _ptr_of(U):

@@ -81,6 +81,76 @@ def test_face_flux_bitwise(mhd, riemann, glm, jump):
     assert np.array_equal(Fo, Fg), np.abs(Fo - Fg).max()
 
 
+def _fast_ops_inputs(n=1 << 21, seed=7):
+    rng = np.random.default_rng(seed)
+    m = n // 4
+    wide = lambda: rng.choice([-1.0, 1.0], m) * 10.0 ** rng.uniform(-320, 308, m)
+    mid = lambda: rng.choice([-1.0, 1.0], m) * 10.0 ** rng.uniform(-6, 6, m)
+    bits = lambda: rng.integers(0, 2**64, m, dtype=np.uint64, endpoint=False).view(np.float64)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+                        1.7976931348623157e308, 1.0, -1.0, 2.0, 0.5, 1.0 - 2**-53, 1.0 + 2**-52, 3.0,
+                        np.nextafter(2.0, 0.0), 1e-300, 1e300, 4.0e-310], dtype=np.float64)
+    sa, sb = np.meshgrid(special, special)
+    # operands of the face solve: positive, O(1) to O(1e6), plus the all-ones mantissas
+    pos = 10.0 ** rng.uniform(-4, 6, m)
+    ones = (np.uint64(0x3FFFFFFFFFFFFFFF) - rng.integers(0, 1 << 12, m).astype(np.uint64)).view(np.float64)
+    a = np.concatenate([wide(), mid(), bits(), pos, sa.ravel(), ones])
+    b = np.concatenate([wide(), mid(), bits(), ones, sb.ravel(), pos])
+    return a, b
+
+
+def test_fast_div_sqrt_bitwise(mhd):
+    """The branch-free reciprocal / division / square-root sequences of the face solve equal the
+    IEEE operators bitwise wherever their range test passes, and the device IEEE operators equal
+    numpy's (correctly rounded) results."""
+    import torch
+    a, b = _fast_ops_inputs()
+    out, ok = mhd.debug_fast_ops(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    out, ok = out.cpu().numpy(), ok.cpu().numpy()
+    with np.errstate(all="ignore"):
+        ref = [1.0 / b, a / b, np.sqrt(a), np.abs(a) / b]
+    b_normal_pos = (b >= 2.2250738585072014e-308) & np.isfinite(b)
+    for j in range(4):
+        fast, ieee = out[:, 2 * j], out[:, 2 * j + 1]
+        both_nan = np.isnan(ieee) & np.isnan(ref[j])
+        assert np.array_equal(ieee.view(np.uint64)[~both_nan], ref[j].view(np.uint64)[~both_nan]), j
+        sel = (ok >> j) & 1 == 1
+        if j == 3:  # |a| / b is defined for positive normal b (a checked square root)
+            sel &= b_normal_pos
+            assert np.all(sel[(a == 0) & b_normal_pos])  # zero numerators stay on the fast path
+        assert np.array_equal(fast[sel].view(np.uint64), ieee[sel].view(np.uint64)), j
+    # the range tests reject only rare operands: every positive O(1e-4..1e6) one passes
+    n4 = (1 << 21) // 4
+    pos = slice(3 * n4, 4 * n4)
+    assert np.all(ok[pos] == 15), np.unique(ok[pos], return_counts=True)
+
+
+@pytest.mark.parametrize("limiter,stepper", [(I.MC, I.RK2), (I.WENOZ, I.RK3)])
+def test_exact_resolve_path_parity(mhd, limiter, stepper):
+    """Faces whose branch-free operators fail a range test are re-solved with the IEEE operators
+    (k_stage's out-of-line exact path).  Here the lower half in z is at rest with gamma p = Bx^2,
+    B = (1, 0, 0): on its x faces the fast-speed discriminant is exactly 0 and sqrt(0) is outside
+    the fast range, so every such face takes the exact path; the upper half is a moving state.
+    The run must still equal the oracle bitwise."""
+    p = I.Problem("exact_path", (16, 16, 32), gamma=2.0, limiter=limiter, stepper=stepper)
+    X, Y, Z = I.mesh(p)
+    tp = 2.0 * math.pi
+    low = Z < 0.5
+    rho = np.where(low, 1.0 + 0.3 * np.sin(tp * X) * np.cos(tp * Y), 1.0)
+    vx = np.where(low, 0.0, -0.5 * np.sin(tp * Y))
+    vy = np.where(low, 0.0, 0.5 * np.sin(tp * X))
+    vz = np.where(low, 0.0, 0.05 * np.sin(tp * Z))
+    by = np.where(low, 0.0, 0.3 * np.sin(tp * X))
+    bz = np.where(low, 0.0, 0.2 * np.cos(tp * Y))
+    U0 = I.prim_to_cons_ic(p, rho, vx, vy, vz, 0.5, 1.0, by, bz)
+    # the premise: in the lower half p = (gamma-1)((E - ke) - me) = 0.5 exactly, so gamma p = Bx^2
+    # and the discriminant (a2 - b2)^2 + 4 a2 bt2 of every x face there is exactly 0
+    pr = (p.gamma - 1.0) * ((U0[4] - 0.0) - 0.5 * ((U0[5] * U0[5] + U0[6] * U0[6]) + U0[7] * U0[7]))
+    assert np.all(pr[low] == 0.5) and np.all(p.gamma * pr[low] == U0[5][low] ** 2)
+    res = run_both(mhd, p, U0, 6)
+    assert_parity(*res)
+
+
 # ---------------------------------------------------------------------------------------------
 # whole runs
 # ---------------------------------------------------------------------------------------------
