@@ -114,7 +114,8 @@ int mhd_nccl_get_unique_id(uint8_t out[128]);
 
 /* Validates the arguments (MHD_E_ARG), plans the slab, allocates the two padded state
  * arrays (U^n and U*; a third with MHD_RK3) on the device and, for nranks > 1, creates the NCCL communicator
- * (collective).  gamma > 1, 0 < cfl < 1.  *out receives the context (NULL on failure). */
+ * (collective).  gamma > 1, 0 < cfl < 1, each active extent >= 4, nx * ny * 9 < 2^31 (32-bit
+ * offsets within a z plane).  *out receives the context (NULL on failure). */
 int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
                const mhd_scheme* scheme, const mhd_dist* dist, mhd_ctx** out);
 

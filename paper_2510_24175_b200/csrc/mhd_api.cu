@@ -445,6 +445,10 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     delete c;
     return MHD_E_ARG;
   }
+  if (grid->n[0] * grid->n[1] * 9 >= (1LL << 31)) {  // the kernels keep 32-bit offsets within a z plane
+    delete c;
+    return MHD_E_ARG;
+  }
   c->dim = nact;
   c->dxmin = INFINITY;
   for (int d = 0; d < c->dim; ++d) c->dxmin = c->dx[d] < c->dxmin ? c->dx[d] : c->dxmin;

@@ -36,8 +36,8 @@ namespace mhd {
 // indexing helpers
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ int wrap_index(int i, int n, int bclo, int bchi) {
-  if (i < 0) return bclo == 0 ? ((i % n) + n) % n : 0;
-  if (i >= n) return bchi == 0 ? i % n : n - 1;
+  if (i < 0) return bclo == 0 ? (i + n >= 0 ? i + n : ((i % n) + n) % n) : 0;  // (% only when n < halo)
+  if (i >= n) return bchi == 0 ? (i - n < n ? i - n : i % n) : n - 1;
   return i;
 }
 
@@ -46,6 +46,20 @@ __device__ __forceinline__ void load_cell(const double* __restrict__ U, size_t p
                                           size_t cell, double* u) {
 #pragma unroll
   for (int f = 0; f < NV; ++f) u[f] = __ldg(U + plane_off + f * fstride + cell);
+}
+
+// the NV fields of one cell: p points at field 0, fields are fs elements apart (the stage
+// kernel keeps 32-bit field offsets from a per-plane 64-bit pointer: one IMAD.WIDE per load)
+template <typename T>
+__device__ __forceinline__ T* opaque(T* p) {  // hides the derivation of p: kept as a 64-bit base
+  asm("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
+template <int NV>
+__device__ __forceinline__ void load_fields(const double* __restrict__ p, int fs, double* u) {
+  p = opaque(p);
+#pragma unroll
+  for (int f = 0; f < NV; ++f) u[f] = __ldg(p + f * fs);
 }
 
 __device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
@@ -99,11 +113,10 @@ __device__ __forceinline__ bool gather_xy(const double* Vc, int d, int row, int 
 }
 
 template <int NV>
-__device__ __forceinline__ void convert_at(const double* __restrict__ Ucol, size_t fstride, double gm1, double pf,
+__device__ __forceinline__ void convert_at(const double* __restrict__ Ucol, int fs, double gm1, double pf,
                                            double* v) {
   double u[NV];
-#pragma unroll
-  for (int f = 0; f < NV; ++f) u[f] = __ldg(Ucol + f * fstride);
+  load_fields<NV>(Ucol, fs, u);
   cons2prim<NV>(u, v, gm1, pf);
 }
 
@@ -111,31 +124,31 @@ __device__ __forceinline__ void convert_at(const double* __restrict__ Ucol, size
 // (Ucol: the column's cell in storage plane 0): the same conversions and reconstructions as
 // the marching path, which carries V+(k) in shared memory instead.
 template <int NV, int REC>
-__device__ __forceinline__ void gather_z(const double* __restrict__ Ucol, size_t pstride, size_t fstride, int k,
+__device__ __forceinline__ void gather_z(const double* __restrict__ Ucol, size_t pstride, int fs, int k,
                                          double gm1, double pf, double* wl, double* wr) {
   constexpr int LIM = REC == 0 ? 0 : 1;
   double qp[NV], qm[NV];
   auto at = [&](int kk) { return Ucol + (ptrdiff_t)kk * (ptrdiff_t)pstride; };
   if constexpr (REC == 2) {
     double q0[NV], q1[NV], q2[NV], q3[NV], q4[NV];
-    convert_at<NV>(at(k - 2), fstride, gm1, pf, q0);
-    convert_at<NV>(at(k - 1), fstride, gm1, pf, q1);
-    convert_at<NV>(at(k), fstride, gm1, pf, q2);
-    convert_at<NV>(at(k + 1), fstride, gm1, pf, q3);
-    convert_at<NV>(at(k + 2), fstride, gm1, pf, q4);
+    convert_at<NV>(at(k - 2), fs, gm1, pf, q0);
+    convert_at<NV>(at(k - 1), fs, gm1, pf, q1);
+    convert_at<NV>(at(k), fs, gm1, pf, q2);
+    convert_at<NV>(at(k + 1), fs, gm1, pf, q3);
+    convert_at<NV>(at(k + 2), fs, gm1, pf, q4);
     weno_cell<NV>(q0, q1, q2, q3, q4, qp, qm);
     to_normal<NV, 2>(qp, wl);
-    convert_at<NV>(at(k + 3), fstride, gm1, pf, q0);
+    convert_at<NV>(at(k + 3), fs, gm1, pf, q0);
     weno_cell<NV>(q1, q2, q3, q4, q0, qp, qm);
     to_normal<NV, 2>(qm, wr);
   } else {
     double q0[NV], q1[NV], q2[NV];
-    convert_at<NV>(at(k - 1), fstride, gm1, pf, q0);
-    convert_at<NV>(at(k), fstride, gm1, pf, q1);
-    convert_at<NV>(at(k + 1), fstride, gm1, pf, q2);
+    convert_at<NV>(at(k - 1), fs, gm1, pf, q0);
+    convert_at<NV>(at(k), fs, gm1, pf, q1);
+    convert_at<NV>(at(k + 1), fs, gm1, pf, q2);
     plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
     to_normal<NV, 2>(qp, wl);
-    convert_at<NV>(at(k + 2), fstride, gm1, pf, q0);
+    convert_at<NV>(at(k + 2), fs, gm1, pf, q0);
     plm_cell<NV, LIM>(q1, q2, q0, qp, qm);
     to_normal<NV, 2>(qm, wr);
   }
@@ -151,9 +164,9 @@ struct FaceOut {
 };
 template <int NV, int RS, int REC, int PH, int PW, int HY, int G>
 __device__ __noinline__ FaceOut<NV> exact_face(StageConsts c, const double* Vc, const double* Ucol, size_t pstride,
-                                               size_t fstride, int kplane, int d, int row, int col) {
+                                               int fs, int kplane, int d, int row, int col) {
   double vl[NV], vr[NV];
-  if (d == 2) gather_z<NV, REC>(Ucol, pstride, fstride, kplane, c.gm1, c.p_floor, vl, vr);
+  if (d == 2) gather_z<NV, REC>(Ucol, pstride, fs, kplane, c.gm1, c.p_floor, vl, vr);
   else gather_xy<NV, REC, PH, PW, HY, G>(Vc, d, row, col, vl, vr);
   FaceOut<NV> o;
   bool unused = true;
@@ -230,8 +243,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int gx = x0 + tx, gy = y0 + ty;
   const bool own = cellw && gx < nx && gy < ny;
-  const size_t fstride = (size_t)nx * ny;
-  const size_t pstride = fstride * NV;
+  const int fs = nx * ny;  // field stride in elements (mhd_create bounds nx*ny*nvar below 2^31)
+  const size_t pstride = (size_t)fs * NV;
   const int kb = a.zb + blockIdx.z * a.kz;  // this CTA's z chunk inside [zb, ze)
   const int ke = min(kb + a.kz, a.ze);
   // rare events (floors, fallbacks, HLL fallbacks, bad cells) go to shared-memory counters by
@@ -247,8 +260,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // own-cell offset (x, y wrapped for ragged lanes: they compute a valid duplicate and never store)
   const int wx = wrap_index(gx, nx, a.bcx[0], a.bcx[1]);
   const int wy = (DIM >= 2) ? wrap_index(gy, ny, a.bcy[0], a.bcy[1]) : 0;
-  const size_t own_cell = (size_t)wy * nx + wx;
-  auto plane_off = [&](int k) -> size_t { return (size_t)(k + a.gz) * pstride; };
+  const int own_cell = wy * nx + wx;
+  // 64-bit pointers to storage plane 0 of the interior; plane k starts k * pstride further
+  const double* __restrict__ U0p = a.Uin + (size_t)a.gz * pstride;
+  const double* __restrict__ Ucol = U0p + own_cell;  // the own column
+  auto at = [&](const double* base, int k) { return base + (ptrdiff_t)k * (ptrdiff_t)pstride; };
   auto glin = [&](int k) -> unsigned long long {
     return ((unsigned long long)(a.zoff + k) * (unsigned long long)ny + (unsigned long long)gy) * (unsigned long long)nx +
            (unsigned long long)gx;
@@ -257,7 +273,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // (interior cell, stage) that counts floors and checks validity
   auto convert_own = [&](int k, double* v, bool count) {
     double u[NV];
-    load_cell<NV>(a.Uin, plane_off(k), fstride, own_cell, u);
+    load_fields<NV>(at(Ucol, k), fs, u);
     const bool fl = cons2prim<NV>(u, v, c.gm1, c.p_floor);
     if (count && own) {
       if (fl) atomicAdd(&s_cnt[0], 1);
@@ -268,7 +284,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     double u[NV];
     const int ix = wrap_index(x, nx, a.bcx[0], a.bcx[1]);
     const int iy = (DIM >= 2) ? wrap_index(y, ny, a.bcy[0], a.bcy[1]) : 0;
-    load_cell<NV>(a.Uin, plane_off(k), fstride, (size_t)iy * nx + ix, u);
+    load_fields<NV>(at(U0p, k) + (iy * nx + ix), fs, u);
     cons2prim<NV>(u, v, c.gm1, c.p_floor);
   };
   auto store_vc = [&](int r, int col, const double* v) {  // r: 0..PH-1, col: 0..PW-1
@@ -341,11 +357,14 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     if (DIM == 3 && cellw) {
       // latency hiding: own column of plane k+3 (first touched next iteration) into L2; own
       // cell of planes k+1, k+2 (the z job) and of plane k (update; U^n in stage 2) into L1
+      const double* p2 = opaque(at(Ucol, k + G + 1 < nzl + a.gz ? k + G + 1 : k));
+      const double* p1 = opaque(at(Ucol, k + G));
+      const double* pn = opaque(at(a.Un + (size_t)a.gz * pstride + own_cell, k));
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
-        prefetch_l2(a.Uin + plane_off(k + G + 1 < nzl + a.gz ? k + G + 1 : k) + f * fstride + own_cell);
-        prefetch_l1(a.Uin + plane_off(k + G) + f * fstride + own_cell);
-        if (full && a.mode != 0) prefetch_l1(a.Un + plane_off(k) + f * fstride + own_cell);
+        prefetch_l2(p2 + f * fs);
+        prefetch_l1(p1 + f * fs);
+        if (full && a.mode != 0) prefetch_l1(pn + f * fs);
       }
     }
     if (!WZ && full && !cellw) {
@@ -456,8 +475,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       if (!ok) {
         // a range test of the branch-free operators failed (rare): the plain operators on the
         // same face, its two states re-derived from shared memory (x, y) or the planes (z)
-        const FaceOut<NV> o = exact_face<NV, RS, REC, PH, PW, HY, G>(c, Vc, a.Uin + own_cell + (size_t)a.gz * pstride,
-                                                                     pstride, fstride, k, d, row, col);
+        const FaceOut<NV> o = exact_face<NV, RS, REC, PH, PW, HY, G>(c, Vc, Ucol, pstride, fs, k, d, row, col);
 #pragma unroll
         for (int f = 0; f < NV; ++f) fn[f] = o.f[f];
         fell = o.fell;
@@ -489,14 +507,17 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads of U
     // and U^n follow the barrier (held across it they would spill; both planes were prefetched
     // into L1 at the top of the iteration).
-    const size_t off = plane_off(k) + (size_t)gy * nx + gx;
     __syncthreads();
-    if (own) {
+    if (own) {  // (own: the cell is not wrapped, own_cell = gy * nx + gx)
+      const size_t off = (size_t)a.gz * pstride + own_cell;
+      const double* pu = opaque(at(a.Uin + off, k));
+      const double* pn = opaque(at(a.Un + off, k));
+      double* po = opaque(a.Uout + off + (ptrdiff_t)k * (ptrdiff_t)pstride);
       double u0[NV], un[NV];
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
-        u0[f] = __ldg(a.Uin + off + f * fstride);
-        un[f] = (a.mode != 0) ? a.Un[off + f * fstride] : 0.0;
+        u0[f] = __ldg(pu + f * fs);
+        un[f] = (a.mode != 0) ? pn[f * fs] : 0.0;
       }
       const double* fzn = Fz + ((k + 1) & 1) * S::nCol;
       const double* fzo = Fz + (k & 1) * S::nCol;
@@ -510,7 +531,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         if (a.mode == 1) v = 0.5 * (un[f] + s);                    // RK2: U^{n+1} = (U^n + U**)/2
         else if (a.mode == 2) v = (a.wa * un[f]) + (a.wb * s);     // RK3: (a U^n) + (b S(U))
         if (NV > 8 && f == NV - 1 && a.last) v = v * c.damp;       // GLM damping once per step
-        a.Uout[off + f * fstride] = v;
+        po[f * fs] = v;
       }
     }
     // ---- advance the plane window (3D).  No barrier before the load: the update reads only
