@@ -135,9 +135,11 @@ static void fill_ghosts(const orc_config* c, const grid_t* G, double* Up) {
 /* ------------------------------------------------------------------------ */
 double orc_wenoz(double a, double b, double c, double d, double e) {
   const double eps = 1e-40;
-  const double t0 = (a - 2.0 * b) + c, u0 = (a - 4.0 * b) + 3.0 * c;
-  const double t1 = (b - 2.0 * c) + d, u1 = b - d;
-  const double t2 = (c - 2.0 * d) + e, u2 = (3.0 * c - 4.0 * d) + e;
+  /* the indicators' terms in a mirror-symmetric association: W(e,d,c,b,a) forms the same
+     t, u (u1 negated) in reverse order (R31) */
+  const double t0 = (a + c) - 2.0 * b, u0 = (a + 3.0 * c) - 4.0 * b;
+  const double t1 = (b + d) - 2.0 * c, u1 = b - d;
+  const double t2 = (c + e) - 2.0 * d, u2 = (3.0 * c + e) - 4.0 * d;
   const double b0 = (13.0 / 12.0) * (t0 * t0) + 0.25 * (u0 * u0);
   const double b1 = (13.0 / 12.0) * (t1 * t1) + 0.25 * (u1 * u1);
   const double b2 = (13.0 / 12.0) * (t2 * t2) + 0.25 * (u2 * u2);

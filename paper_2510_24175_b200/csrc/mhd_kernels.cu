@@ -195,7 +195,7 @@ struct StageSmem {
   static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vpz, Fz[0], Fz[1] each
   static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
   static constexpr int nFx = NV * TY * (TX + 1);
-  static constexpr int nXP = NV * TY;  // q+ (x) of cell x0-1 per row, from the edge warp (PLM)
+  static constexpr int nXP = NV * TY;  // q+ (x) of cell x0-1 per row, from the edge warp
   static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx + nXP);
 };
 
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   double* Fz = Vpz + S::nCol;        // [2][NV][NC] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
   double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
   double* Fx = Fy + S::nFy;          // [NV][TY][TX+1] x-face fluxes of plane k
-  double* XP = Fx + S::nFx;          // [NV][TY] q+ along x of cell x0-1 of every row (PLM)
+  double* XP = Fx + S::nFx;          // [NV][TY] q+ along x of cell x0-1 of every row
 
   const StageConsts& c = a.c;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -367,20 +367,35 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         if (full && a.mode != 0) prefetch_l1(pn + f * fs);
       }
     }
-    if (!WZ && full && !cellw) {
-      // PLM x faces: the cell warps reconstruct each cell once along x and pass q+ to the next
+    if (full && !cellw) {
+      // x faces: the cell warps reconstruct each cell once along x and pass q+ to the next
       // lane; the edge warp supplies q+ of the cells x0-1 (lane 0's left neighbours) and then
       // releases the cell warps' x jobs (named barrier 1: producer arrive / consumer sync)
       if (tx < TY) {
-        double qa[NV], qb[NV], qc[NV], qp[NV], qm[NV];
+        double qa[NV], qb[NV], qc[NV], qp[NV];
+        if constexpr (WZ) {
+          double qaa[NV], qcc[NV];
 #pragma unroll
-        for (int f = 0; f < NV; ++f) {
-          const double* base = Vc + (f * PH + tx + HY) * PW + G - 1;
-          qa[f] = base[-1];
-          qb[f] = base[0];
-          qc[f] = base[1];
+          for (int f = 0; f < NV; ++f) {
+            const double* base = Vc + (f * PH + tx + HY) * PW + G - 1;
+            qaa[f] = base[-2];
+            qa[f] = base[-1];
+            qb[f] = base[0];
+            qc[f] = base[1];
+            qcc[f] = base[2];
+          }
+          weno_side<NV, true>(qaa, qa, qb, qc, qcc, qp);
+        } else {
+          double qm[NV];
+#pragma unroll
+          for (int f = 0; f < NV; ++f) {
+            const double* base = Vc + (f * PH + tx + HY) * PW + G - 1;
+            qa[f] = base[-1];
+            qb[f] = base[0];
+            qc[f] = base[1];
+          }
+          plm_cell<NV, LIM>(qa, qb, qc, qp, qm);
         }
-        plm_cell<NV, LIM>(qa, qb, qc, qp, qm);
 #pragma unroll
         for (int f = 0; f < NV; ++f) XP[f * TY + tx] = qp[f];
       }
@@ -446,17 +461,31 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
           to_normal<NV, 2>(qm, wr);
 #pragma unroll
           for (int f = 0; f < NV; ++f) Vpz[f * NC + tid] = wp[f];
-        } else if (!WZ && job == 3) {
+        } else if (job == 3) {
           // x face tx-1/2 (cell warps): own cell reconstructed once, left state from lane tx-1
           double qa[NV], qb[NV], qc[NV], qp[NV];
+          if constexpr (WZ) {
+            double qaa[NV], qcc[NV];
 #pragma unroll
-          for (int n = 0; n < NV; ++n) {
-            const double* base = Vc + (n * PH + row + HY) * PW + col + G;
-            qa[n] = base[-1];
-            qb[n] = base[0];
-            qc[n] = base[1];
+            for (int n = 0; n < NV; ++n) {
+              const double* base = Vc + (n * PH + row + HY) * PW + col + G;
+              qaa[n] = base[-2];
+              qa[n] = base[-1];
+              qb[n] = base[0];
+              qc[n] = base[1];
+              qcc[n] = base[2];
+            }
+            fb = weno_cell<NV>(qaa, qa, qb, qc, qcc, qp, wr);
+          } else {
+#pragma unroll
+            for (int n = 0; n < NV; ++n) {
+              const double* base = Vc + (n * PH + row + HY) * PW + col + G;
+              qa[n] = base[-1];
+              qb[n] = base[0];
+              qc[n] = base[1];
+            }
+            fb = plm_cell<NV, LIM>(qa, qb, qc, qp, wr);
           }
-          fb = plm_cell<NV, LIM>(qa, qb, qc, qp, wr);
           asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // XP written by the edge warp
 #pragma unroll
           for (int n = 0; n < NV; ++n) {
