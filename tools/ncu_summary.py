@@ -15,7 +15,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
 
 
-def to_json(path, out_json, cells):
+def to_json(path, out_json, cells, which="stage 1 (7th stage launch: after 3 warm-up steps)"):
     """one-kernel summary used by bench.py's roofline.traffic (profiles/ncu_stage_summary.json)"""
     import json
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -37,7 +37,7 @@ def to_json(path, out_json, cells):
          "registers_per_thread": g("launch__registers_per_thread"),
          "warp_instructions": g("smsp__inst_executed.sum"),
          "thread_instructions_per_cell": g("smsp__inst_executed.sum") * 32 / cells,
-         "stage_of_launch": "stage 1 (7th stage launch: after 3 warm-up steps)"}
+         "stage_of_launch": which}
     json.dump(d, open(out_json, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
@@ -62,7 +62,7 @@ def main(path):
 
 if __name__ == "__main__":
     if sys.argv[1] == "--json":
-        to_json(sys.argv[2], sys.argv[3], float(sys.argv[4]))
+        to_json(sys.argv[2], sys.argv[3], float(sys.argv[4]), *sys.argv[5:6])
     else:
         for p in sys.argv[1:]:
             main(p)
