@@ -140,20 +140,9 @@ def build_problem(workload: str, n_gpus: int, n: int, scheme: str = "plm-rk2"):
     return p
 
 
-def build_ic(workload: str, p, z0: int, z1: int, chunk: int = 64):
-    """initial condition of global planes [z0, z1), generated in z chunks into one array (keeps
-    the host peak near the array size for 1024^3)"""
+def build_ic(workload: str, p, z0: int, z1: int):
     from paper_2510_24175_b200 import inputs as I
-    if p.ct and workload == "cpa3d":  # face fields from the edge vector potential (whole grid)
-        assert (z0, z1) == (0, p.n[2])
-        return I.cpa_3d_ct_ic(p)
-    fn = {"ot3d": I.orszag_tang_3d_ic, "blast3d": I.blast_3d_ic, "cpa3d": I.cpa_3d_ic}[workload]
-    pg = p.replace(ct=0, glm=1) if p.ct else p  # OT and blast fields are face-exact: CT takes fields 0..7
-    U = np.empty((p.nvar, z1 - z0, p.n[1], p.n[0]), dtype=np.float64)
-    for a in range(z0, z1, chunk):
-        b = min(z1, a + chunk)
-        U[:, a - z0:b - z0] = fn(pg, z_range=(a, b))[:p.nvar]
-    return U
+    return I.workload_ic(workload, p, z0, z1)
 
 
 def cpu_info():

@@ -165,6 +165,13 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]);
 
+/* A sub-box of the current state: off/ext in global interior cell coordinates, inside this
+ * rank's local block (mhd_local_box), every ext >= 1.  U: [nvar][ext_z][ext_y][ext_x], host
+ * (on_device == 0) or device memory, owned by the caller.  Synchronising; MHD_E_ARG for a box
+ * outside the block, MHD_E_STATE before mhd_set_state.  (For sampled checks and I/O of states
+ * too large to copy out whole.) */
+int mhd_get_state_box(mhd_ctx* ctx, const int64_t off[3], const int64_t ext[3], double* U, int32_t on_device);
+
 /* Counters and the unphysical-state record.  On one GPU the counters are read back from the
  * device (synchronising) and include every completed step; with NCCL slabs they are the global
  * sums reduced by the last mhd_compute_dt (the collective). */

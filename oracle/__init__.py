@@ -211,6 +211,19 @@ def face_flux(problem, VL, VR, ch):
     return F, int(nfb)
 
 
+def compute_dt(problem, U):
+    """c.13 on a contiguous interior U without copying it (for full-size states): (dt, ch)."""
+    cfg = make_config(problem)
+    assert U.flags.c_contiguous and U.dtype == np.float64
+    dt, ch = C.c_double(), C.c_double()
+    cnt = Counters()
+    lib().orc_counters_reset(C.byref(cnt))
+    rc = lib().orc_compute_dt(C.byref(cfg), _ptr(U), C.byref(dt), C.byref(ch), C.byref(cnt))
+    if rc:
+        raise OracleError(rc, cnt)
+    return dt.value, ch.value
+
+
 def stage(problem, U, dt, ch):
     cfg = make_config(problem)
     U = np.ascontiguousarray(U, dtype=np.float64)

@@ -665,6 +665,26 @@ int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
   return MHD_OK;
 }
 
+int mhd_get_state_box(mhd_ctx* c, const int64_t off[3], const int64_t ext[3], double* U, int32_t on_device) {
+  if (!c || !off || !ext || !U) return MHD_E_ARG;
+  if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  const int64_t lo[3] = {0, 0, c->zoff}, hi[3] = {c->nx, c->ny, c->zoff + c->nzl};
+  for (int d = 0; d < 3; ++d)
+    if (ext[d] < 1 || off[d] < lo[d] || off[d] + ext[d] > hi[d]) return set_err(c, MHD_E_ARG, "box outside the local block");
+  const size_t pe = plane_elems(c), fs = (size_t)c->nx * c->ny;
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  for (int f = 0; f < c->nv; ++f)
+    for (int64_t z = 0; z < ext[2]; ++z) {
+      const double* src = c->U0 + (size_t)(off[2] - c->zoff + z + c->gz) * pe + (size_t)f * fs +
+                          (size_t)off[1] * c->nx + (size_t)off[0];
+      double* dst = U + ((size_t)f * ext[2] + (size_t)z) * (size_t)(ext[1] * ext[0]);
+      CUDA_OR_RETURN(c, cudaMemcpy2DAsync(dst, (size_t)ext[0] * sizeof(double), src, (size_t)c->nx * sizeof(double),
+                                          (size_t)ext[0] * sizeof(double), (size_t)ext[1], kind, c->stream));
+    }
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  return MHD_OK;
+}
+
 int mhd_compute_dt(mhd_ctx* c, double* dt) {
   if (!c || !dt) return MHD_E_ARG;
   if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)

@@ -360,3 +360,20 @@ CONFIGS = {
     "ot3d_1024": (lambda: orszag_tang_3d(1024), orszag_tang_3d_ic),
     "cpa3d_256": (lambda: cpa_3d(256), cpa_3d_ic),
 }
+
+
+def workload_ic(workload: str, p: Problem, z0: int = 0, z1: int = -1, chunk: int = 64) -> np.ndarray:
+    """Initial condition of global planes [z0, z1) of a bench workload ("ot3d", "blast3d",
+    "cpa3d"), generated in z chunks into one array (keeps the host peak near the array size
+    for 1024^3)."""
+    z1 = p.n[2] if z1 < 0 else z1
+    if p.ct and workload == "cpa3d":  # face fields from the edge vector potential (whole grid)
+        assert (z0, z1) == (0, p.n[2])
+        return cpa_3d_ct_ic(p)
+    fn = {"ot3d": orszag_tang_3d_ic, "blast3d": blast_3d_ic, "cpa3d": cpa_3d_ic}[workload]
+    pg = p.replace(ct=0, glm=1) if p.ct else p  # OT and blast fields are face-exact: CT takes fields 0..7
+    U = np.empty((p.nvar, z1 - z0, p.n[1], p.n[0]), dtype=np.float64)
+    for a in range(z0, z1, chunk):
+        b = min(z1, a + chunk)
+        U[:, a - z0:b - z0] = fn(pg, z_range=(a, b))[:p.nvar]
+    return U

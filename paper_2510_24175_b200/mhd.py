@@ -28,7 +28,8 @@ _NAMES = {0: "MHD_OK", 1: "MHD_E_ARG", 2: "MHD_E_STATE", 3: "MHD_E_CUDA", 4: "MH
 EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_box", "mhd_device_bytes",
            "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
-           "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops")
+           "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
+           "mhd_get_state_box")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -85,6 +86,8 @@ def load() -> C.CDLL:
     L.mhd_device_bytes.argtypes = [P, C.POINTER(C.c_size_t)]
     L.mhd_set_state.argtypes = [P, P, C.c_int32]
     L.mhd_get_state.argtypes = [P, P, C.c_int32]
+    if hasattr(L, "mhd_get_state_box"):  # (absent from older builds used in A/B runs)
+        L.mhd_get_state_box.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, C.c_int32]
     L.mhd_compute_dt.argtypes = [P, C.POINTER(C.c_double)]
     L.mhd_step.argtypes = [P, C.c_double]
     L.mhd_get_diag.argtypes = [P, C.POINTER(Diag)]
@@ -215,6 +218,13 @@ class Solver:
         if nbytes != int(np.prod(self.local_shape)) * 8:
             raise ValueError(f"output must have shape {self.local_shape}")
         self._check(self._L.mhd_get_state(self._h, C.c_void_p(p), dev))
+        return out
+
+    def get_state_box(self, off, ext) -> np.ndarray:
+        """State of the global cell box [off, off+ext) (x, y, z) as [nvar][ez][ey][ex] (host)."""
+        out = np.empty((self.problem.nvar, ext[2], ext[1], ext[0]), dtype=np.float64)
+        o, e = (C.c_int64 * 3)(*off), (C.c_int64 * 3)(*ext)
+        self._check(self._L.mhd_get_state_box(self._h, o, e, C.c_void_p(out.ctypes.data), 0))
         return out
 
     def compute_dt(self) -> float:

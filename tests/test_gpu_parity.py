@@ -179,6 +179,30 @@ def test_ot2d(mhd, n):
     assert_parity(*run_both(mhd, p, I.orszag_tang_2d_ic(p), 120))
 
 
+@pytest.mark.slow
+def test_ot2d_512_config_to_t05(mhd):
+    """BASELINE configs[1] (2D Orszag-Tang 512^2, PLM+HLLD+GLM, to t = 0.5): element by element
+    equal to the oracle for the first 100 steps at full size; the GPU run to t = 0.5 then
+    conserves mass, momentum, energy and B to round-off (periodic) and keeps the point symmetry
+    of the vortex (scalars even, vectors odd about the centre)."""
+    p = I.orszag_tang_2d(512)
+    U0 = I.orszag_tang_2d_ic(p)
+    assert_parity(*run_both(mhd, p, U0, 100))
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    log = s.run(100000, 0.5)
+    U = s.get_state()
+    s.destroy()
+    assert abs(float(np.sum(log)) - 0.5) <= 1e-12 and len(log) > 1000
+    for f in range(8):
+        scale = np.abs(U0[f]).sum()
+        assert abs(U[f].sum() - U0[f].sum()) <= 1e-11 * scale, f
+    rot = lambda a: a[:, ::-1, ::-1]
+    for f, sgn in ((0, 1), (4, 1), (1, -1), (2, -1), (5, -1), (6, -1)):
+        assert np.abs(U[f] - sgn * rot(U[f])).max() <= 1e-8 * np.abs(U[f]).max(), f
+    assert np.abs(U[3]).max() == 0 and np.abs(U[7]).max() == 0
+
+
 @pytest.mark.parametrize("limiter,riemann", [(I.MC, I.HLLD), (I.MINMOD, I.HLLD), (I.MC, I.HLL)])
 def test_ot3d_small(mhd, limiter, riemann):
     p = I.orszag_tang_3d(32, limiter=limiter, riemann=riemann)
@@ -306,6 +330,70 @@ def test_ot3d_256_full_size_parity(mhd):
     U0 = I.orszag_tang_3d_ic(p)
     res = run_both(mhd, p, U0, 2)
     assert_parity(*res)
+
+
+def _sampled_step_parity(mhd, workload, p, samples, halo=4):
+    """One step of a full-size BASELINE config on the GPU, in bench.py's launch configuration,
+    checked on sampled cells: the dt equals the oracle's on the whole state (bitwise), and each
+    sampled cell equals the oracle's step of its (2*halo+1)^3 neighbourhood (the PLM-RK2 update
+    of a cell reads U^n within +-4 cells; outflow ghosts of the small box reach only its outer
+    cells) with the whole-domain dt and c_h."""
+    U0 = I.workload_ic(workload, p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    dt_g = s.compute_dt()
+    dt_o, ch_o = oracle.compute_dt(p, U0)
+    assert dt_g == dt_o, (dt_g, dt_o)
+    s.step(dt_g)
+    w = 2 * halo + 1
+    dx = [(p.hi[d] - p.lo[d]) / p.n[d] for d in range(3)]
+    sub = p.replace(n=(w, w, w), lo=(0.0, 0.0, 0.0), hi=(w * dx[0], w * dx[1], w * dx[2]),
+                    bc=(I.OUTFLOW, I.OUTFLOW, I.OUTFLOW))
+    assert all((sub.hi[d] - sub.lo[d]) / w == dx[d] for d in range(3))  # identical dt/dx
+    for (x, y, z) in samples:
+        ix = [(x + o) % p.n[0] for o in range(-halo, halo + 1)]
+        iy = [(y + o) % p.n[1] for o in range(-halo, halo + 1)]
+        iz = [(z + o) % p.n[2] for o in range(-halo, halo + 1)]
+        box = np.ascontiguousarray(U0[:, iz][:, :, iy][:, :, :, ix])
+        o = oracle.Oracle(sub, box)
+        o.step(dt_o, ch_o)
+        want = o.U[:, halo, halo, halo]
+        got = s.get_state_box((x, y, z), (1, 1, 1))[:, 0, 0, 0]
+        assert np.array_equal(got, want), ((x, y, z), got - want)
+    s.destroy()
+
+
+def _edge_and_random_cells(n, k, rng, extra=()):
+    nx, ny, nz = n
+    cells = [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (0, ny - 1, 1), (nx - 1, 0, nz - 2), (1, ny // 2, 0),
+             (nx // 2, 1, nz - 1)]
+    cells += [tuple(int(v) for v in (rng.integers(nx), rng.integers(ny), rng.integers(nz))) for _ in range(k)]
+    return cells + list(extra)
+
+
+@pytest.mark.slow
+def test_blast_512_full_size_sampled(mhd):
+    """BASELINE configs[3] per GPU (blast 512^3, one rank's slab): one step, sampled cells,
+    including cells on the blast front."""
+    p = I.blast_3d(512)
+    rng = np.random.default_rng(11)
+    front = []
+    for _ in range(24):  # cells within a few cells of the r = 0.1 sphere
+        v = rng.normal(size=3)
+        v = 0.5 + (0.1 + rng.uniform(-3, 3) / 512) * v / np.linalg.norm(v)
+        front.append(tuple(int(np.clip(c * 512, 0, 511)) for c in v))
+    _sampled_step_parity(mhd, "blast3d", p, _edge_and_random_cells(p.n, 16, rng, front))
+
+
+@pytest.mark.slow
+def test_ot3d_1024_full_size_sampled(mhd):
+    """BASELINE configs[4] at P = 1 (OT-3D 1024^3, 155 GB on the GPU, 77 GB host state): one
+    step, sampled cells (the oracle cannot hold two copies of the whole state)."""
+    import psutil
+    if psutil.virtual_memory().total < 120 << 30:
+        pytest.skip("needs a host with >= 120 GB of RAM for the 77 GB 1024^3 state")
+    p = I.orszag_tang_3d(1024)
+    _sampled_step_parity(mhd, "ot3d", p, _edge_and_random_cells(p.n, 40, np.random.default_rng(12)))
 
 
 # ---------------------------------------------------------------------------------------------

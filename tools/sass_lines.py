@@ -56,5 +56,5 @@ for loc, c in byline.most_common(top):
             if os.path.exists(cand):
                 srcs[f] = open(cand).read().splitlines()
     s = srcs.get(f, [""] * (ln + 1))[ln - 1].strip()[:72] if f in srcs else ""
-    ops = ", ".join(f"{o}:{100 * v / c:.0f}%" for o, v in byop[loc].most_common(3))
+    ops = ", ".join(f"{o}:{100 * v / max(c, 1):.0f}%" for o, v in byop[loc].most_common(3))
     print(f"{100 * c / tot:5.1f}% stall {100 * bysmp[loc] / max(tots, 1):5.1f}% {f}:{ln:<4d} {s:72s} [{ops}]")
