@@ -165,6 +165,23 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]);
 
+/* Pipelined host I/O (pinned host buffers, one full state each, caller-owned; the buffer must
+ * stay valid and unmodified until mhd_io_join or the next call that waits on it):
+ *  - mhd_set_state_async: starts the host->device copy of U ([nvar][z][y][x], as mhd_set_state)
+ *    on the library's upload stream and returns; the next mhd_compute_dt / mhd_step /
+ *    mhd_get_state* makes it the state (unpack + validation on the context's stream; an
+ *    unphysical cell is reported by the next synchronising call, as a dt-pass error).
+ *  - mhd_get_state_async: packs the current state (after all enqueued steps) into a staging
+ *    array and starts its device->host copy into U on the download stream; returns at once.
+ *  - mhd_io_join: makes the context's stream wait for every started copy (no host wait), so an
+ *    event recorded on it afterwards, or cudaStreamSynchronize, covers them.
+ * The copies of step n+1's input and step n-1's output overlap step n's kernels.  Two staging
+ * arrays (2 x nvar x cells x 8 bytes) are allocated on first use (MHD_E_NOMEM if they do not
+ * fit).  Not for in-process slab groups. */
+int mhd_set_state_async(mhd_ctx* ctx, const double* U);
+int mhd_get_state_async(mhd_ctx* ctx, double* U);
+int mhd_io_join(mhd_ctx* ctx);
+
 /* A sub-box of the current state: off/ext in global interior cell coordinates, inside this
  * rank's local block (mhd_local_box), every ext >= 1.  U: [nvar][ext_z][ext_y][ext_x], host
  * (on_device == 0) or device memory, owned by the caller.  Synchronising; MHD_E_ARG for a box

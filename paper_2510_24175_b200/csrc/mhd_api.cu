@@ -63,6 +63,14 @@ struct mhd_ctx {
   int sticky = MHD_OK;
   mhd_diag diag;
   char err[512];
+  // pipelined host I/O (mhd_set_state_async / mhd_get_state_async / mhd_io_join): staging
+  // arrays in the ABI layout, copied on their own streams so the copies of one step overlap the
+  // compute of its neighbours
+  double* io_in = nullptr;
+  double* io_out = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in_copied = nullptr, ev_in_free = nullptr, ev_out_packed = nullptr, ev_out_copied = nullptr;
+  bool in_pending = false;
   // kernel timing (mhd_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -391,6 +399,46 @@ int reset_device_records(mhd_ctx* c) {
   return MHD_OK;
 }
 
+int io_setup(mhd_ctx* c) {
+  if (c->io_in) return MHD_OK;
+  const size_t bytes = plane_elems(c) * (size_t)c->nzl * sizeof(double);
+  if (cudaMalloc(&c->io_in, bytes) != cudaSuccess || cudaMalloc(&c->io_out, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    if (c->io_in) cudaFree(c->io_in);
+    c->io_in = c->io_out = nullptr;
+    return set_err(c, MHD_E_NOMEM, "async I/O: no room for two staging arrays (%zu bytes each)", bytes);
+  }
+  CUDA_OR_RETURN(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  CUDA_OR_RETURN(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_in_copied, &c->ev_in_free, &c->ev_out_packed, &c->ev_out_copied})
+    CUDA_OR_RETURN(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return MHD_OK;
+}
+
+// a pending mhd_set_state_async takes effect on the compute stream: wait for its copy, unpack
+// into U^n, validate (reported by the next synchronising call as an unphysical cell of the dt
+// pass, like the synchronous path's), reset the per-state records
+int apply_input(mhd_ctx* c) {
+  if (!c->in_pending) return MHD_OK;
+  c->in_pending = false;
+  c->sticky = MHD_OK;
+  c->ch_valid = false;
+  c->has_state = false;
+  c->diag.first_bad_cell = -1;
+  c->diag.bad_stage = -1;
+  int rc = reset_device_records(c);
+  if (rc) return rc;
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_in_copied, 0));
+  cudaError_t e = mhd::launch_pack(c->io_in, c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, 1, c->nsm, c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "pack: %s", cudaGetErrorString(e));
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_in_free, c->stream));
+  e = mhd::launch_validate(c->U0, c->nv, c->nx, c->ny, c->nzl, c->gz, c->zoff, c->gamma - 1.0, c->dbuf + 5, c->nsm,
+                           c->stream, c->scheme.ct ? 0 : 1);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "validate: %s", cudaGetErrorString(e));
+  c->has_state = true;
+  return MHD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -617,6 +665,7 @@ int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
 
 int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
   if (!c || !U) return MHD_E_ARG;
+  c->in_pending = false;  // supersedes a pending mhd_set_state_async
   const size_t n = plane_elems(c) * (size_t)c->nzl;
   c->sticky = MHD_OK;
   c->ch_valid = false;
@@ -654,6 +703,8 @@ int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
 
 int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
   if (!c || !U) return MHD_E_ARG;
+  int rc = apply_input(c);
+  if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
   const size_t n = plane_elems(c) * (size_t)c->nzl;
   double* dst = on_device ? U : c->U1;
@@ -665,8 +716,50 @@ int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
   return MHD_OK;
 }
 
+int mhd_set_state_async(mhd_ctx* c, const double* U) {
+  if (!c || !U) return MHD_E_ARG;
+  if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)
+    return set_err(c, MHD_E_STATE, "in-process slab group: use mhd_set_state");
+  int rc = io_setup(c);
+  if (rc) return rc;
+  const size_t bytes = plane_elems(c) * (size_t)c->nzl * sizeof(double);
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->h2d, c->ev_in_free, 0));  // the previous input was unpacked
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->io_in, U, bytes, cudaMemcpyHostToDevice, c->h2d));
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_in_copied, c->h2d));
+  c->in_pending = true;
+  return MHD_OK;
+}
+
+int mhd_get_state_async(mhd_ctx* c, double* U) {
+  if (!c || !U) return MHD_E_ARG;
+  int rc = apply_input(c);
+  if (rc) return rc;
+  if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  rc = io_setup(c);
+  if (rc) return rc;
+  const size_t bytes = plane_elems(c) * (size_t)c->nzl * sizeof(double);
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_out_copied, 0));  // the previous output left
+  cudaError_t e = mhd::launch_pack(c->U0, c->io_out, c->nv, c->nx, c->ny, c->nzl, c->gz, 0, c->nsm, c->stream);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "unpack: %s", cudaGetErrorString(e));
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_out_packed, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->d2h, c->ev_out_packed, 0));
+  CUDA_OR_RETURN(c, cudaMemcpyAsync(U, c->io_out, bytes, cudaMemcpyDeviceToHost, c->d2h));
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_out_copied, c->d2h));
+  return MHD_OK;
+}
+
+int mhd_io_join(mhd_ctx* c) {
+  if (!c) return MHD_E_ARG;
+  if (!c->io_in) return MHD_OK;
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_in_copied, 0));
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_out_copied, 0));
+  return MHD_OK;
+}
+
 int mhd_get_state_box(mhd_ctx* c, const int64_t off[3], const int64_t ext[3], double* U, int32_t on_device) {
   if (!c || !off || !ext || !U) return MHD_E_ARG;
+  int rc = apply_input(c);
+  if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
   const int64_t lo[3] = {0, 0, c->zoff}, hi[3] = {c->nx, c->ny, c->zoff + c->nzl};
   for (int d = 0; d < 3; ++d)
@@ -689,7 +782,9 @@ int mhd_compute_dt(mhd_ctx* c, double* dt) {
   if (!c || !dt) return MHD_E_ARG;
   if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)
     return set_err(c, MHD_E_STATE, "in-process slab group: use mhd_group_compute_dt");
-  int rc = check_sticky(c);
+  int rc = apply_input(c);
+  if (rc) return rc;
+  rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
   rc = reduce_and_read(c);
@@ -711,7 +806,9 @@ int mhd_step(mhd_ctx* c, double dt) {
   if (!c) return MHD_E_ARG;
   if (c->transport == MHD_TRANSPORT_LOCAL && c->nranks > 1)
     return set_err(c, MHD_E_STATE, "in-process slab group: use mhd_group_step");
-  int rc = check_sticky(c);
+  int rc = apply_input(c);
+  if (rc) return rc;
+  rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
   if (!(dt > 0.0) || !std::isfinite(dt)) return set_err(c, MHD_E_ARG, "dt must be positive and finite");
@@ -849,6 +946,14 @@ const char* mhd_last_error(const mhd_ctx* c) { return c ? c->err : "null context
 void mhd_destroy(mhd_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->h2d) cudaStreamSynchronize(c->h2d);
+  if (c->d2h) cudaStreamSynchronize(c->d2h);
+  if (c->io_in) cudaFree(c->io_in);
+  if (c->io_out) cudaFree(c->io_out);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  for (cudaEvent_t e : {c->ev_in_copied, c->ev_in_free, c->ev_out_packed, c->ev_out_copied})
+    if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);

@@ -29,7 +29,7 @@ EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_
            "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
            "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
-           "mhd_get_state_box")
+           "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -88,6 +88,10 @@ def load() -> C.CDLL:
     L.mhd_get_state.argtypes = [P, P, C.c_int32]
     if hasattr(L, "mhd_get_state_box"):  # (absent from older builds used in A/B runs)
         L.mhd_get_state_box.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, C.c_int32]
+    if hasattr(L, "mhd_io_join"):
+        L.mhd_set_state_async.argtypes = [P, P]
+        L.mhd_get_state_async.argtypes = [P, P]
+        L.mhd_io_join.argtypes = [P]
     L.mhd_compute_dt.argtypes = [P, C.POINTER(C.c_double)]
     L.mhd_step.argtypes = [P, C.c_double]
     L.mhd_get_diag.argtypes = [P, C.POINTER(Diag)]
@@ -219,6 +223,25 @@ class Solver:
             raise ValueError(f"output must have shape {self.local_shape}")
         self._check(self._L.mhd_get_state(self._h, C.c_void_p(p), dev))
         return out
+
+    def _host_ptr(self, U):
+        p, dev, nbytes = _ptr_of(U)
+        if dev or nbytes != int(np.prod(self.local_shape)) * 8:
+            raise ValueError(f"need a host buffer of shape {self.local_shape}")
+        return p
+
+    def set_state_async(self, U) -> None:
+        """Start the upload of U (pinned host memory: torch.Tensor.pin_memory()); it becomes the
+        state at the next compute_dt / step / get_state*.  Keep U alive and unchanged until io_join."""
+        self._check(self._L.mhd_set_state_async(self._h, C.c_void_p(self._host_ptr(U))))
+
+    def get_state_async(self, out) -> None:
+        """Start the download of the current state into `out` (pinned host); complete after
+        io_join() and a synchronisation of the stream."""
+        self._check(self._L.mhd_get_state_async(self._h, C.c_void_p(self._host_ptr(out))))
+
+    def io_join(self) -> None:
+        self._check(self._L.mhd_io_join(self._h))
 
     def get_state_box(self, off, ext) -> np.ndarray:
         """State of the global cell box [off, off+ext) (x, y, z) as [nvar][ez][ey][ex] (host)."""

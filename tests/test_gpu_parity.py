@@ -258,6 +258,44 @@ def test_state_roundtrip_host_and_device(mhd):
     s.destroy()
 
 
+def test_async_io_pipeline_equals_sync(mhd):
+    """set_state_async / get_state_async / io_join (the pipelined e2e path) give the same dt
+    sequence and states as the synchronous calls, step by step."""
+    import torch
+    p = I.orszag_tang_3d(24).replace(n=(24, 20, 16))
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    ref = mhd.Solver(p)
+    s = mhd.Solver(p)
+    Uh = torch.from_numpy(U0).pin_memory()
+    outs = [torch.empty_like(Uh).pin_memory() for _ in range(3)]
+    ins = [Uh]  # (the uploads read these until io_join: keep them alive)
+    want = []
+    for i in range(3):
+        ref.set_state(np.ascontiguousarray(U0) if i == 0 else want[-1])
+        dt_r = ref.compute_dt()
+        ref.step(dt_r)
+        want.append(ref.get_state())
+        if i > 0:
+            ins.append(torch.from_numpy(want[i - 1]).pin_memory())
+        s.set_state_async(ins[-1])
+        assert s.compute_dt() == dt_r
+        s.step(dt_r)
+        s.get_state_async(outs[i])
+    s.io_join()
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert np.array_equal(outs[i].numpy(), want[i]), i
+    # an unphysical state uploaded asynchronously is reported by the next synchronising call
+    bad = U0.copy()
+    bad[0, 3, 4, 5] = -1.0
+    ins.append(torch.from_numpy(bad).pin_memory())
+    s.set_state_async(ins[-1])
+    with pytest.raises(mhd.MhdError):
+        s.compute_dt()
+    s.destroy()
+    ref.destroy()
+
+
 def test_unphysical_state_rejected_and_sticky(mhd):
     p = I.orszag_tang_3d(16)
     U = I.orszag_tang_3d_ic(p)
