@@ -77,7 +77,7 @@ typedef struct {
   double p_floor;    /* pressure floor on primitives (counted), R16 */
   int32_t ct;        /* 1: constrained transport instead of GLM: glm = 0,
                         nvar = 8 with fields 5..7 = face-centred b_x (x-face i-1/2), b_y (j-1/2),
-                        b_z (k-1/2); 3D, periodic on every axis, one GPU (nranks = 1) */
+                        b_z (k-1/2); 3D, periodic on every axis, one GPU or z slabs */
   int32_t reserved;
 } mhd_scheme;
 

@@ -283,6 +283,18 @@ void prof_drain(mhd_ctx* c) {
   c->ev_kind.clear();
 }
 
+// CT: the z ghost planes of U complete before the launch (periodic copy on one GPU; the NCCL
+// halo on slabs, waited for on the compute stream: the CT stage has no interior/boundary split)
+int ct_fill_ghosts(mhd_ctx* c, double* U) {
+  int rc = fill_z_ghosts_local(c, U);
+  if (rc) return rc;
+  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
+    if ((rc = exchange_nccl(c, U))) return rc;
+    CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+  }
+  return MHD_OK;
+}
+
 int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   const StagePlan sp = stage_plan(c, stage);
   StageArgs a;
@@ -331,6 +343,8 @@ int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.ny = c->ny;
   a.nz = c->nzl;
   a.gz = c->gz;
+  a.G = c->gz - 1;
+  a.zoff = c->zoff;
   a.stage = stage;
   a.mode = sp.mode;
   a.last = sp.last;
@@ -525,8 +539,8 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->nv = 8 + c->scheme.glm;
   c->rank = dist ? dist->rank : 0;
   c->nranks = dist ? dist->nranks : 1;
-  if (c->scheme.ct) {  // CT: periodic on every axis, one GPU (R32)
-    bool ok = c->nranks == 1;
+  if (c->scheme.ct) {  // CT: periodic on every axis (R32), one GPU or z slabs
+    bool ok = true;
     for (int d = 0; d < 3; ++d) ok = ok && c->bc_lo[d] == MHD_BC_PERIODIC;
     if (!ok) {
       delete c;
@@ -555,6 +569,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->nzl = (int)(c->n[2] / c->nranks);
   c->zoff = (long long)c->nzl * c->rank;
   c->gz = c->dim == 3 ? (c->scheme.limiter == MHD_LIM_WENOZ ? 3 : 2) : 0;
+  if (c->scheme.ct) c->gz += 1;  // the topmost reconstructed plane needs b_z one plane further
   if (c->dim == 3 && c->nzl < c->gz) {
     delete c;
     return MHD_E_ARG;
@@ -787,6 +802,7 @@ int mhd_compute_dt(mhd_ctx* c, double* dt) {
   rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
+  if (c->scheme.ct && (rc = ct_fill_ghosts(c, c->U0))) return rc;  // cell-centred B_z needs plane nz
   rc = reduce_and_read(c);
   if (rc) return rc;
   double M, S;
@@ -820,8 +836,10 @@ int mhd_step(mhd_ctx* c, double dt) {
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
   if (c->scheme.ct) {
-    for (int stage = 1; stage <= nstages(c); ++stage)
+    for (int stage = 1; stage <= nstages(c); ++stage) {
+      if ((rc = ct_fill_ghosts(c, stage_plan(c, stage).in))) return rc;
       if ((rc = run_ct_stage(c, stage, k))) return rc;
+    }
     c->ch_valid = false;
     c->diag.steps += 1;
     return MHD_OK;
@@ -880,6 +898,12 @@ int mhd_group_compute_dt(mhd_ctx* const* ctxs, int32_t n, double* dt) {
   int rc = check_group(ctxs, n);
   if (rc || !dt) return rc ? rc : MHD_E_ARG;
   double M = 0.0, S = 0.0;
+  if (ctxs[0]->scheme.ct) {  // CT: U^n ghost planes (cell-centred B_z of the last plane)
+    for (int r = 0; r < n; ++r) {
+      if ((rc = fill_z_ghosts_local(ctxs[r], ctxs[r]->U0))) return rc;
+      if (n > 1 && (rc = exchange_local(ctxs[r], 1))) return rc;
+    }
+  }
   for (int r = 0; r < n; ++r) {  // exact maxima: the order over slabs does not matter
     mhd_ctx* c = ctxs[r];
     if ((rc = reduce_and_read(c))) return rc;
@@ -913,7 +937,7 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
     for (int r = 0; r < n; ++r) {
       mhd_ctx* c = ctxs[r];
       const StageConsts k = make_consts(c, dt, c->ch);
-      if ((rc = run_stage(c, stage, k, 0, c->nzl))) return rc;
+      if ((rc = c->scheme.ct ? run_ct_stage(c, stage, k) : run_stage(c, stage, k, 0, c->nzl))) return rc;
     }
   }
   for (int r = 0; r < n; ++r) {

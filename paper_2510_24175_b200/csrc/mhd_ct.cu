@@ -2,7 +2,10 @@
 //
 // The paper's weak-scaling runs keep div B = 0 with constrained transport (
 // Evans & Hawley 1988, Londrillo & Del Zanna 2004).  State: rho, m, E cell-centred, b_x / b_y /
-// b_z on the x / y / z faces (face i-1/2 / j-1/2 / k-1/2 of cell (i,j,k)), 3D periodic, one GPU.
+// b_z on the x / y / z faces (face i-1/2 / j-1/2 / k-1/2 of cell (i,j,k)), 3D periodic, on one GPU
+// or z slabs.  x/y are wrapped by index; z reads ghost planes (gz = G + 1 per side, G the
+// reconstruction half-width: the topmost V plane needs b_z one plane further), filled by a
+// periodic copy on one GPU or the slab halo exchange before every stage and dt pass.
 // Per RK stage three kernels:
 //   k_ct_prim    cell-centred B = face average, cons->prim -> V (8 fields)
 //   k_ct_face<D> reconstruction along D, normal field = the face value, face solve -> F_D (the
@@ -25,10 +28,17 @@ __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >
 struct CtIdx {
   int nx, ny, nz, gz;
   size_t fs, ps;  // field stride (nx*ny), plane stride (8*fs)
+  // cell (i, j, k) of field f: x, y wrapped (periodic), k in [-gz, nz + gz) (ghost planes)
   __device__ size_t at(int f, int i, int j, int k) const {
-    return (size_t)(wrapi(k, nz) + gz) * ps + (size_t)f * fs + (size_t)wrapi(j, ny) * nx + wrapi(i, nx);
+    return (size_t)(k + gz) * ps + (size_t)f * fs + (size_t)wrapi(j, ny) * nx + wrapi(i, nx);
   }
 };
+// decode q in [0, nx*ny*nk) into (i, j, k0 + kk)
+__device__ __forceinline__ void ct_decode(size_t q, int nx, int ny, int k0, int& i, int& j, int& k) {
+  i = (int)(q % nx);
+  j = (int)((q / nx) % ny);
+  k = k0 + (int)(q / ((size_t)nx * ny));
+}
 
 __device__ __forceinline__ void ct_cell_cons(const double* __restrict__ U, const CtIdx& X, int i, int j, int k,
                                              double* w) {
@@ -39,20 +49,25 @@ __device__ __forceinline__ void ct_cell_cons(const double* __restrict__ U, const
   w[7] = 0.5 * (__ldg(U + X.at(7, i, j, k)) + __ldg(U + X.at(7, i, j, k + 1)));
 }
 
-// 1-2: cell-centred primitives of every cell (V uses the same padded layout, ghost planes unused)
+// 1-2: cell-centred primitives of the planes [-G, nz + G) (V: the same padded layout); floors
+// and bad cells are counted on the interior planes only (the owner rule)
 __global__ void __launch_bounds__(256) k_ct_prim(CtArgs a) {
   const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
-  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  const size_t n = (size_t)a.nx * a.ny * (a.nz + 2 * a.G);
   int floors = 0;
   unsigned long long bad = ULLONG_MAX;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    int i, j, k;
+    ct_decode(q, a.nx, a.ny, -a.G, i, j, k);
+    const bool interior = k >= 0 && k < a.nz;
     double u[8], w[8], v[8];
 #pragma unroll
     for (int f = 0; f < 8; ++f) u[f] = __ldg(a.Uin + X.at(f, i, j, k));
-    if (bad_state<8>(u)) bad = min(bad, (unsigned long long)q);
+    if (interior && bad_state<8>(u))
+      bad = min(bad, (unsigned long long)(((a.zoff + k) * a.ny + j) * (long long)a.nx + i));
     ct_cell_cons(a.Uin, X, i, j, k, w);
-    floors += cons2prim<8>(w, v, a.c.gm1, a.c.p_floor) ? 1 : 0;
+    const bool fl = cons2prim<8>(w, v, a.c.gm1, a.c.p_floor);
+    floors += (fl && interior) ? 1 : 0;
 #pragma unroll
     for (int f = 0; f < 8; ++f) a.V[X.at(f, i, j, k)] = v[f];
   }
@@ -60,15 +75,20 @@ __global__ void __launch_bounds__(256) k_ct_prim(CtArgs a) {
   if (bad != ULLONG_MAX) atomicMin(a.bad + a.stage, bad);
 }
 
-// 3-4: face i-1/2 (along D) of every cell: reconstruction, staggered normal field, face solve
+// 3-4: face i-1/2 (along D) of every cell: reconstruction, staggered normal field, face solve.
+// x/y faces on the planes [-1, nz] (the edge EMFs of the slab's end planes use the faces of the
+// planes beyond), z faces k-1/2 for k in [0, nz]; counters for the faces of interior cells
 template <int D, int RS, int REC>
 __global__ void __launch_bounds__(128) k_ct_face(CtArgs a) {
   const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
-  const size_t n = (size_t)a.nx * a.ny * a.nz;
+  const int k0 = D == 2 ? 0 : -1;
+  const size_t n = (size_t)a.nx * a.ny * (a.nz + (D == 2 ? 1 : 2));
   constexpr int oi = D == 0, oj = D == 1, ok = D == 2;
   int fbs = 0, hlls = 0;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    int i, j, k;
+    ct_decode(q, a.nx, a.ny, k0, i, j, k);
+    const bool interior = k >= 0 && k < a.nz;
     double c[6][8];  // cells -3..+2 relative to cell (i,j,k) along D (PLM uses -2..+1)
     constexpr int lo = REC == 2 ? -3 : -2, hi = REC == 2 ? 2 : 1;
 #pragma unroll
@@ -84,14 +104,15 @@ __global__ void __launch_bounds__(128) k_ct_face(CtArgs a) {
       plm_cell<8, REC>(c[1], c[2], c[3], vl, tmp);
       fb = plm_cell<8, REC>(c[2], c[3], c[4], tmp, vr);
     }
-    fbs += fb ? 1 : 0;
+    fbs += (fb && interior) ? 1 : 0;
     const double b = __ldg(a.Uin + X.at(5 + D, i, j, k));  // the staggered normal field of this face
     vl[5 + D] = b;
     vr[5 + D] = b;
     double wl[8], wr[8], fn[8], fx[8];
     to_normal<8, D>(vl, wl);
     to_normal<8, D>(vr, wr);
-    hlls += face_flux<8, RS>(wl, wr, a.c, fn);
+    const int fell = face_flux<8, RS>(wl, wr, a.c, fn);
+    hlls += (fell && interior) ? 1 : 0;
     from_normal<8, D>(fn, fx);
     double* F = a.F[D];
 #pragma unroll
@@ -124,7 +145,8 @@ __global__ void __launch_bounds__(256) k_ct_update(CtArgs a) {
   const size_t n = (size_t)a.nx * a.ny * a.nz;
   const double* lam = a.c.lam;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    int i, j, k;
+    ct_decode(q, a.nx, a.ny, 0, i, j, k);
     double s[8];
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
@@ -153,14 +175,15 @@ __global__ void __launch_bounds__(256) k_ct_update(CtArgs a) {
 
 template <int RS, int REC>
 static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st) {
-  const size_t n = (size_t)a.nx * a.ny * a.nz;
-  const unsigned g256 = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 16);
-  const unsigned g128 = (unsigned)std::min<size_t>((n + 127) / 128, (size_t)nsm * 32);
-  k_ct_prim<<<g256, 256, 0, st>>>(a);
-  k_ct_face<0, RS, REC><<<g128, 128, 0, st>>>(a);
-  k_ct_face<1, RS, REC><<<g128, 128, 0, st>>>(a);
-  k_ct_face<2, RS, REC><<<g128, 128, 0, st>>>(a);
-  k_ct_update<<<g256, 256, 0, st>>>(a);
+  const size_t pc = (size_t)a.nx * a.ny;
+  auto grid = [&](size_t n, int bs, int per_sm) {
+    return (unsigned)std::max<size_t>(1, std::min<size_t>((n + bs - 1) / bs, (size_t)nsm * per_sm));
+  };
+  k_ct_prim<<<grid(pc * (a.nz + 2 * a.G), 256, 16), 256, 0, st>>>(a);
+  k_ct_face<0, RS, REC><<<grid(pc * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
+  k_ct_face<1, RS, REC><<<grid(pc * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
+  k_ct_face<2, RS, REC><<<grid(pc * (a.nz + 1), 128, 32), 128, 0, st>>>(a);
+  k_ct_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -183,11 +206,12 @@ __global__ void __launch_bounds__(256) k_ct_dt(DtArgs a) {
   double M = 0.0, Sx = 0.0;
   unsigned long long bad = ULLONG_MAX;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / ((size_t)a.nx * a.ny));
+    int i, j, k;
+    ct_decode(q, a.nx, a.ny, 0, i, j, k);
     double u[8], v[8];
-    ct_cell_cons(a.U, X, i, j, k, u);
+    ct_cell_cons(a.U, X, i, j, k, u);  // (b_z of plane k + 1: the ghost plane above the last one)
     if (bad_state<8>(u)) {
-      bad = min(bad, (unsigned long long)q);
+      bad = min(bad, (unsigned long long)(((a.zoff + k) * a.ny + j) * (long long)a.nx + i));
       continue;
     }
     cons2prim<8>(u, v, a.gm1, a.p_floor);

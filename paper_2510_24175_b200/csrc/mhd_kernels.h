@@ -42,14 +42,16 @@ struct DtArgs {
 
 cudaError_t launch_stage(int dim, int nv, int riemann, const StageArgs& a, cudaStream_t st);
 
-// constrained transport (mhd_ct.cu): 3D, periodic, one GPU, 8 fields (b on faces)
+// constrained transport (mhd_ct.cu): 3D, periodic, one GPU or z slabs, 8 fields (b on faces)
 struct CtArgs {
-  const double* Uin;  // stage input (padded [z+gz][8][y][x], ghost planes unused: periodic wrap)
+  const double* Uin;  // stage input (padded [z+gz][8][y][x], z ghost planes filled)
   const double* Un;   // U^n for the RK epilogue
   double* Uout;
   double* V;          // scratch: cell-centred primitives
   double* F[3];       // scratch: face fluxes per direction (induction entries = face EMFs)
   int nx, ny, nz, gz;
+  int G;              // reconstruction half-width (2 PLM, 3 WENO-Z); gz = G + 1
+  long long zoff;     // global z offset of this slab (bad-cell indices)
   int stage, mode, last;
   double wa, wb;
   StageConsts c;

@@ -619,3 +619,31 @@ def test_ct_parity(mhd, case):
     res = run_both(mhd, p, U0, n)
     assert_parity(*res)
     assert np.abs(oracle.ct_divb(p, res[2])).max() < 1e-10
+
+
+@pytest.mark.parametrize("case,P", [("plm_rk2", 2), ("plm_rk2", 4), ("wenoz_rk3", 2), ("wenoz_rk3", 3)])
+def test_ct_slab_group_bitwise(mhd, case, P):
+    """CT on z slabs (ghost planes gz = G + 1, halo per stage and per dt pass): P slabs run in
+    one process with the same plan, kernels and z ranges as NCCL ranks equal one domain
+    bitwise, with equal counters (and so the oracle, test_ct_parity)."""
+    from test_oracle_scheme import _random_ct_state
+    if case == "plm_rk2":
+        p = I.orszag_tang_3d(12, limiter=I.MC).replace(n=(20, 14, 24), ct=1, glm=0)
+    else:
+        p = I.orszag_tang_3d(12, limiter=I.WENOZ).replace(n=(16, 12, 24), ct=1, glm=0, stepper=I.RK3)
+    U0 = _random_ct_state(p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(6)
+    U1 = s.get_state()
+    d1 = s.diag()
+    s.destroy()
+    g = mhd.SolverGroup(p, P)
+    g.set_state(U0)
+    logP = g.run(6)
+    UP = g.get_state()
+    dP = g.diag()
+    g.destroy()
+    assert np.array_equal(log1, logP) and np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k], (k, d1[k], dP[k])
