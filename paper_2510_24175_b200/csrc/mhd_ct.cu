@@ -8,8 +8,8 @@
 // periodic copy on one GPU or the slab halo exchange before every stage and dt pass.
 // Per RK stage three kernels:
 //   k_ct_prim    cell-centred B = face average, cons->prim -> V (8 fields)
-//   k_ct_face<D> reconstruction along D, normal field = the face value, face solve -> F_D (the
-//                induction entries are the face EMFs)
+//   k_ct_face_x, k_ct_face_m<D>: reconstruction along D (each cell once), normal field = the face
+//                value, face solve -> F_D (the induction entries are the face EMFs)
 //   k_ct_update  rho, m, E by the flux divergence; b by Stokes with edge EMFs averaged from the
 //                four adjacent face EMFs (arithmetic); the RK epilogue.
 // The arithmetic of every step follows the recipe of DESIGN.md R32 operation for
@@ -75,48 +75,123 @@ __global__ void __launch_bounds__(256) k_ct_prim(CtArgs a) {
   if (bad != ULLONG_MAX) atomicMin(a.bad + a.stage, bad);
 }
 
-// 3-4: face i-1/2 (along D) of every cell: reconstruction, staggered normal field, face solve.
-// x/y faces on the planes [-1, nz] (the edge EMFs of the slab's end planes use the faces of the
-// planes beyond), z faces k-1/2 for k in [0, nz]; counters for the faces of interior cells
-template <int D, int RS, int REC>
-__global__ void __launch_bounds__(128) k_ct_face(CtArgs a) {
-  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
-  const int k0 = D == 2 ? 0 : -1;
-  const size_t n = (size_t)a.nx * a.ny * (a.nz + (D == 2 ? 1 : 2));
+// 3-4: faces along D: reconstruction, staggered normal field, face solve.  x/y faces on the
+// planes [-1, nz] (the edge EMFs of the slab's end planes use the faces of the planes beyond),
+// z faces k-1/2 for k in [0, nz]; counters for the faces of interior cells (the right cell's
+// reconstruction fallback, R17; the solve's HLL fallback).  Every cell is reconstructed once
+// per direction (both states from one WENO-Z indicator set or one PLM slope): the y and z
+// kernels march along D carrying q+ of the previous cell, the x kernel passes q+ to the next
+// lane and solves the faces at 32-cell chunk starts in a second pass.
+
+// both states of cell (i,j,k) along D from V; returns the positivity fallback
+template <int D, int REC>
+__device__ __forceinline__ bool ct_recon(const CtArgs& a, const CtIdx& X, int i, int j, int k, double* qp,
+                                         double* qm) {
   constexpr int oi = D == 0, oj = D == 1, ok = D == 2;
+  constexpr int H = REC == 2 ? 2 : 1;
+  double c[2 * H + 1][8];
+#pragma unroll
+  for (int s = -H; s <= H; ++s)
+#pragma unroll
+    for (int f = 0; f < 8; ++f) c[s + H][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
+  if constexpr (REC == 2) return weno_cell<8>(c[0], c[1], c[2], c[3], c[4], qp, qm);
+  else return plm_cell<8, REC>(c[0], c[1], c[2], qp, qm);
+}
+
+// the face between vl (q+ of the cell before) and vr (q- of cell (i,j,k)) along D: staggered
+// normal field, solve, F_D at (i,j,k); returns the HLL fallback.  vl, vr are modified.
+template <int D, int RS>
+__device__ __forceinline__ int ct_solve_store(const CtArgs& a, const CtIdx& X, double* vl, double* vr, int i, int j,
+                                              int k) {
+  const double b = __ldg(a.Uin + X.at(5 + D, i, j, k));  // the staggered normal field of this face
+  vl[5 + D] = b;
+  vr[5 + D] = b;
+  double wl[8], wr[8], fn[8], fx[8];
+  to_normal<8, D>(vl, wl);
+  to_normal<8, D>(vr, wr);
+  const int fell = face_flux<8, RS>(wl, wr, a.c, fn);
+  from_normal<8, D>(fn, fx);
+  double* F = a.F[D];
+#pragma unroll
+  for (int f = 0; f < 8; ++f) F[X.at(f, i, j, k)] = fx[f];
+  return fell;
+}
+
+constexpr int kCtSeg = 16;  // cells per marching segment (one extra reconstruction per segment)
+
+// y (D = 1) and z (D = 2) faces: a thread marches a segment of one line (lane = x, coalesced)
+template <int D, int RS, int REC>
+__global__ void __launch_bounds__(128) k_ct_face_m(CtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const int nb = D == 1 ? a.nz + 2 : a.ny;     // second line coordinate: k + 1 (y) or j (z)
+  const int nm = D == 1 ? a.ny : a.nz + 1;     // marched faces per line
+  const int nseg = (nm + kCtSeg - 1) / kCtSeg;
+  const size_t n = (size_t)a.nx * nb * nseg;
   int fbs = 0, hlls = 0;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    ct_decode(q, a.nx, a.ny, k0, i, j, k);
-    const bool interior = k >= 0 && k < a.nz;
-    double c[6][8];  // cells -3..+2 relative to cell (i,j,k) along D (PLM uses -2..+1)
-    constexpr int lo = REC == 2 ? -3 : -2, hi = REC == 2 ? 2 : 1;
+    const int i = (int)(q % a.nx);
+    const size_t r = q / a.nx;
+    const int b = (int)(r % nb), sg = (int)(r / nb);
+    const int m0 = sg * kCtSeg, m1 = min(m0 + kCtSeg, nm);
+    auto cell = [&](int m, int& j, int& k) {
+      if (D == 1) { j = m; k = b - 1; } else { j = b; k = m; }
+    };
+    double pl[8], qp[8], qm[8];
+    int j, k;
+    cell(m0 - 1, j, k);
+    ct_recon<D, REC>(a, X, i, j, k, pl, qm);  // q+ of the cell before the segment's first face
+    for (int m = m0; m < m1; ++m) {
+      cell(m, j, k);
+      const bool interior = k >= 0 && k < a.nz;
+      const bool fb = ct_recon<D, REC>(a, X, i, j, k, qp, qm);
+      fbs += (fb && interior) ? 1 : 0;
+      hlls += (ct_solve_store<D, RS>(a, X, pl, qm, i, j, k) && interior) ? 1 : 0;
 #pragma unroll
-    for (int s = lo; s <= hi; ++s)
-#pragma unroll
-      for (int f = 0; f < 8; ++f) c[s + 3][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
-    double vl[8], vr[8], tmp[8];
-    bool fb;
-    if constexpr (REC == 2) {
-      weno_side<8, true>(c[0], c[1], c[2], c[3], c[4], vl);        // left cell: q+
-      fb = weno_side<8, false>(c[1], c[2], c[3], c[4], c[5], vr);  // right cell: q-
-    } else {
-      plm_cell<8, REC>(c[1], c[2], c[3], vl, tmp);
-      fb = plm_cell<8, REC>(c[2], c[3], c[4], tmp, vr);
+      for (int f = 0; f < 8; ++f) pl[f] = qp[f];
     }
-    fbs += (fb && interior) ? 1 : 0;
-    const double b = __ldg(a.Uin + X.at(5 + D, i, j, k));  // the staggered normal field of this face
-    vl[5 + D] = b;
-    vr[5 + D] = b;
-    double wl[8], wr[8], fn[8], fx[8];
-    to_normal<8, D>(vl, wl);
-    to_normal<8, D>(vr, wr);
-    const int fell = face_flux<8, RS>(wl, wr, a.c, fn);
-    hlls += (fell && interior) ? 1 : 0;
-    from_normal<8, D>(fn, fx);
-    double* F = a.F[D];
+  }
+  if (fbs) atomicAdd(a.counters + 1, (unsigned long long)fbs);
+  if (hlls) atomicAdd(a.counters + 2, (unsigned long long)hlls);
+}
+
+// x faces: warps over 32-cell chunks of the rows (j, k), k in [-1, nz]; lane l > 0 takes q+ of
+// cell i-1 from lane l-1; the faces at chunk starts follow in a second pass, one per thread
+template <int RS, int REC>
+__global__ void __launch_bounds__(128) k_ct_face_x(CtArgs a) {
+  const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
+  const int nch = (a.nx + 31) / 32;
+  const size_t items = (size_t)nch * a.ny * (a.nz + 2);
+  const int lane = threadIdx.x & 31;
+  const size_t gw = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  int fbs = 0, hlls = 0;
+  for (size_t w = gw; w < items; w += nw) {  // warp-uniform loop
+    const int cx = (int)(w % nch);
+    const size_t row = w / nch;
+    const int j = (int)(row % a.ny), k = (int)(row / a.ny) - 1;
+    const int i = cx * 32 + lane;  // (i >= nx: a wrapped duplicate, never stored)
+    double qp[8], qm[8], pl[8];
+    const bool fb = ct_recon<0, REC>(a, X, i, j, k, qp, qm);
 #pragma unroll
-    for (int f = 0; f < 8; ++f) F[X.at(f, i, j, k)] = fx[f];
+    for (int f = 0; f < 8; ++f) pl[f] = __shfl_up_sync(0xffffffffu, qp[f], 1);
+    if (lane > 0 && i < a.nx) {
+      const bool interior = k >= 0 && k < a.nz;
+      fbs += (fb && interior) ? 1 : 0;
+      hlls += (ct_solve_store<0, RS>(a, X, pl, qm, i, j, k) && interior) ? 1 : 0;
+    }
+  }
+  const size_t nt = (size_t)gridDim.x * blockDim.x;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < items; q += nt) {  // chunk starts
+    const int cx = (int)(q % nch);
+    const size_t row = q / nch;
+    const int j = (int)(row % a.ny), k = (int)(row / a.ny) - 1;
+    const int i = cx * 32;
+    const bool interior = k >= 0 && k < a.nz;
+    double pl[8], qm[8], t[8];
+    ct_recon<0, REC>(a, X, i - 1, j, k, pl, t);
+    const bool fb = ct_recon<0, REC>(a, X, i, j, k, t, qm);
+    fbs += (fb && interior) ? 1 : 0;
+    hlls += (ct_solve_store<0, RS>(a, X, pl, qm, i, j, k) && interior) ? 1 : 0;
   }
   if (fbs) atomicAdd(a.counters + 1, (unsigned long long)fbs);
   if (hlls) atomicAdd(a.counters + 2, (unsigned long long)hlls);
@@ -180,9 +255,11 @@ static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((n + bs - 1) / bs, (size_t)nsm * per_sm));
   };
   k_ct_prim<<<grid(pc * (a.nz + 2 * a.G), 256, 16), 256, 0, st>>>(a);
-  k_ct_face<0, RS, REC><<<grid(pc * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
-  k_ct_face<1, RS, REC><<<grid(pc * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
-  k_ct_face<2, RS, REC><<<grid(pc * (a.nz + 1), 128, 32), 128, 0, st>>>(a);
+  k_ct_face_x<RS, REC><<<grid((size_t)((a.nx + 31) / 32) * 32 * a.ny * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
+  const size_t segy = (size_t)a.nx * (a.nz + 2) * ((a.ny + kCtSeg - 1) / kCtSeg);
+  const size_t segz = (size_t)a.nx * a.ny * ((a.nz + 1 + kCtSeg - 1) / kCtSeg);
+  k_ct_face_m<1, RS, REC><<<grid(segy, 128, 32), 128, 0, st>>>(a);
+  k_ct_face_m<2, RS, REC><<<grid(segz, 128, 32), 128, 0, st>>>(a);
   k_ct_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
