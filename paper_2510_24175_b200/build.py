@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmhd.so")
-SOURCES = ["mhd_kernels.cu", "mhd_ct.cu", "mhd_api.cu"]
+SOURCES = ["mhd_kernels.cu", "mhd_ct.cu", "mhd_split.cu", "mhd_api.cu"]
 DEPS = SOURCES + ["mhd_device.cuh", "mhd_kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -43,6 +43,9 @@ struct mhd_ctx {
   double* U2 = nullptr;  // RK3 only: U2
   double* ctV = nullptr;                          // CT scratch: primitives
   double* ctF[3] = {nullptr, nullptr, nullptr};   // CT scratch: face fluxes
+  bool split = false;                             // 3D GLM WENO-Z: the five-launch stage (mhd_split.cu)
+  double* spF[3] = {nullptr, nullptr, nullptr};   // split scratch: face fluxes over (nx+1)(ny+1)(nz+1)
+  size_t spF_elems = 0;
   size_t arr_elems = 0;
   unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..8] bad slots, [20] debug
   unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (the first 9 entries)
@@ -360,6 +363,42 @@ int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   return MHD_OK;
 }
 
+// one WENO-Z stage of the 3D GLM path (mhd_split.cu); the z ghost planes of the input are filled
+int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+  const StagePlan sp = stage_plan(c, stage);
+  mhd::SplitArgs a;
+  a.Uin = sp.in;
+  a.Un = c->U0;
+  a.Uout = sp.out;
+  a.V = c->ctV;
+  for (int d = 0; d < 3; ++d) a.F[d] = c->spF[d];
+  a.nx = c->nx;
+  a.ny = c->ny;
+  a.nz = c->nzl;
+  a.gz = c->gz;
+  a.px = mhd::split_row_pitch(c->nx);
+  a.zoff = c->zoff;
+  a.nz_glob = c->n[2];
+  a.bcx[0] = c->bc_lo[0];
+  a.bcx[1] = c->bc_hi[0];
+  a.bcy[0] = c->bc_lo[1];
+  a.bcy[1] = c->bc_hi[1];
+  a.stage = stage;
+  a.mode = sp.mode;
+  a.last = sp.last;
+  a.wa = sp.wa;
+  a.wb = sp.wb;
+  a.c = k;
+  a.counters = c->dbuf + 2;
+  a.bad = c->dbuf + 5;
+  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
+  const int pr = prof_begin(c, 0);
+  cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream);
+  prof_end(c, pr);
+  if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "split stage %d: %s", stage, cudaGetErrorString(e));
+  return MHD_OK;
+}
+
 // dt / c_h maxima of U^n into dbuf[0..1], reduced over ranks; reads back dbuf. Synchronising.
 int reduce_and_read(mhd_ctx* c) {
   CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 2 * sizeof(unsigned long long), c->stream));
@@ -570,6 +609,9 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   c->zoff = (long long)c->nzl * c->rank;
   c->gz = c->dim == 3 ? (c->scheme.limiter == MHD_LIM_WENOZ ? 3 : 2) : 0;
   if (c->scheme.ct) c->gz += 1;  // the topmost reconstructed plane needs b_z one plane further
+  // 3D GLM WENO-Z runs the five-launch stage (MHD_FUSED_WENOZ=1 keeps the fused kernel, for A/B)
+  c->split = c->dim == 3 && !c->scheme.ct && c->scheme.limiter == MHD_LIM_WENOZ && c->nv == mhd::NVS;
+  if (const char* f = getenv("MHD_FUSED_WENOZ")) if (atoi(f) == 1) c->split = false;
   if (c->dim == 3 && c->nzl < c->gz) {
     delete c;
     return MHD_E_ARG;
@@ -610,6 +652,11 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.ct) {
     e2 = cudaMalloc(&c->ctV, c->arr_elems * sizeof(double));
     for (int d = 0; d < 3 && e2 == cudaSuccess; ++d) e2 = cudaMalloc(&c->ctF[d], c->arr_elems * sizeof(double));
+  }
+  if (e1 == cudaSuccess && e2 == cudaSuccess && c->split) {  // V (padded like U) + three face-flux arrays
+    c->spF_elems = (size_t)mhd::split_row_pitch(c->nx) * (c->ny + 1) * (size_t)(c->nzl + 1) * mhd::NVS;
+    e2 = cudaMalloc(&c->ctV, c->arr_elems * sizeof(double));
+    for (int d = 0; d < 3 && e2 == cudaSuccess; ++d) e2 = cudaMalloc(&c->spF[d], c->spF_elems * sizeof(double));
   }
   cudaError_t e4 = cudaMallocHost(&c->hbuf, 24 * sizeof(unsigned long long));
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
@@ -674,7 +721,8 @@ int mhd_local_box(const mhd_ctx* c, int64_t off[3], int64_t ext[3]) {
 
 int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
   if (!c || !bytes) return MHD_E_ARG;
-  *bytes = ((c->U2 ? 3 : 2) + (c->ctV ? 4 : 0)) * c->arr_elems * sizeof(double) + 24 * sizeof(unsigned long long);
+  *bytes = ((c->U2 ? 3 : 2) + (c->ctV ? (c->split ? 1 : 4) : 0)) * c->arr_elems * sizeof(double) +
+           3 * c->spF_elems * sizeof(double) + 24 * sizeof(unsigned long long);
   return MHD_OK;
 }
 
@@ -835,10 +883,10 @@ int mhd_step(mhd_ctx* c, double dt) {
   }
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
-  if (c->scheme.ct) {
+  if (c->scheme.ct || c->split) {
     for (int stage = 1; stage <= nstages(c); ++stage) {
       if ((rc = ct_fill_ghosts(c, stage_plan(c, stage).in))) return rc;
-      if ((rc = run_ct_stage(c, stage, k))) return rc;
+      if ((rc = c->split ? run_split_stage(c, stage, k) : run_ct_stage(c, stage, k))) return rc;
     }
     c->ch_valid = false;
     c->diag.steps += 1;
@@ -937,7 +985,9 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
     for (int r = 0; r < n; ++r) {
       mhd_ctx* c = ctxs[r];
       const StageConsts k = make_consts(c, dt, c->ch);
-      if ((rc = c->scheme.ct ? run_ct_stage(c, stage, k) : run_stage(c, stage, k, 0, c->nzl))) return rc;
+      if ((rc = c->scheme.ct ? run_ct_stage(c, stage, k)
+                             : (c->split ? run_split_stage(c, stage, k) : run_stage(c, stage, k, 0, c->nzl))))
+        return rc;
     }
   }
   for (int r = 0; r < n; ++r) {
@@ -986,8 +1036,10 @@ void mhd_destroy(mhd_ctx* c) {
   if (c->U1) cudaFree(c->U1);
   if (c->U2) cudaFree(c->U2);
   if (c->ctV) cudaFree(c->ctV);
-  for (int d = 0; d < 3; ++d)
+  for (int d = 0; d < 3; ++d) {
     if (c->ctF[d]) cudaFree(c->ctF[d]);
+    if (c->spF[d]) cudaFree(c->spF[d]);
+  }
   if (c->dbuf) cudaFree(c->dbuf);
   if (c->hbuf) cudaFreeHost(c->hbuf);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -59,6 +59,27 @@ struct CtArgs {
   unsigned long long* bad;       // [4] per stage
 };
 cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st);
+
+// the WENO-Z stage of the 3D GLM path as five launches (mhd_split.cu)
+constexpr int NVS = 9;
+struct SplitArgs {
+  const double* Uin;  // stage input (padded [z+gz][9][y][x], z ghost planes filled, gz = 3)
+  const double* Un;   // U^n for the RK epilogue
+  double* Uout;
+  double* V;          // scratch: primitives, padded like U
+  double* F[3];       // scratch: face fluxes [k][f][j][i], row pitch px, ny + 1 rows, k in [0, nz]
+  int nx, ny, nz, gz;
+  int px;             // split_row_pitch(nx)
+  long long zoff, nz_glob;
+  int bcx[2], bcy[2];
+  int stage, mode, last;
+  double wa, wb;
+  StageConsts c;
+  unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
+  unsigned long long* bad;       // [4] per stage
+};
+cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st);
+inline int split_row_pitch(int nx) { return (nx + 1 + 31) / 32 * 32; }
 cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st);
 int stage_tile_rows(int dim, int limiter);
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter);  // resident CTAs per SM of the stage kernel
