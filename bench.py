@@ -311,8 +311,10 @@ def main():
                     "frac": bytes_launch / stage_avg_s / 1e9 / pk.get("hbm_gbs", 6537.3), "peak_kind": pk_kind,
                     "algorithmic_bytes_per_launch": bytes_launch},
             "ncu": ncu or None}
-    if args.scheme != "plm-rk2":
-        roof["kernel"] = "k_stage (fused cons2prim + WENO-Z + GLM + HLLD + flux divergence + RK3 update)"
+    if args.scheme != "plm-rk2":  # 3D GLM WENO-Z: the split stage (mhd_split.cu); ncu: its x-face kernel
+        roof["kernel"] = ("split WENO-Z stage (k_sp_prim + k_sp_face_x + k_sp_face_m<1> + k_sp_face_m<2> + "
+                          "k_sp_update; stage_ms and achieved are per 5-launch stage)")
+        roof["traffic"] = None
     if ct:  # the timed unit is a 5-launch stage, not the fused kernel: report the stage time only
         roof = {"bound": "alu", "achieved": None, "peak": fp64_peak, "unit": "TFLOP/s", "frac": None,
                 "traffic": None, "kernel": "CT stage (k_ct_prim + 3 x k_ct_face + k_ct_update)",

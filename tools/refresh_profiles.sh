@@ -18,14 +18,17 @@ python tools/ncu_summary.py --json $O/ncu_stage_plm.ncu-rep profiles/ncu_stage_s
 python tools/ncu_summary.py $O/ncu_stage_plm.ncu-rep > $O/ncu_stage_plm_summary.txt 2>&1
 cp profiles/ncu_stage_summary.json $O/
 
-# 2. WENO-Z + RK3 stage kernel (stage 1 of the 4th step = 10th stage launch)
+# 2. WENO-Z + RK3 split stage: its x-face kernel (the 10th k_sp_face_x launch = stage 1 of step 4)
 $B --scheme wenoz-rk3 --steps 2 --warmup 3 --no-e2e --no-cpu > $O/plain_wz.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:k_stage --launch-skip 9 --launch-count 1 \
-    -o $O/ncu_stage_wenoz $B --scheme wenoz-rk3 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_full_wz.log 2>&1
-python tools/ncu_summary.py --json $O/ncu_stage_wenoz.ncu-rep profiles/ncu_stage_summary_wenoz-rk3.json $CELLS \
-  "stage 1 (10th stage launch: after 3 warm-up RK3 steps)" > /dev/null
-python tools/ncu_summary.py $O/ncu_stage_wenoz.ncu-rep > $O/ncu_stage_wenoz_summary.txt 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_sp_face_x --launch-skip 9 --launch-count 1 \
+    -o $O/ncu_spx_wenoz $B --scheme wenoz-rk3 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_full_wz.log 2>&1
+python tools/ncu_summary.py --json $O/ncu_spx_wenoz.ncu-rep profiles/ncu_stage_summary_wenoz-rk3.json $CELLS \
+  "k_sp_face_x of stage 1 (10th launch: after 3 warm-up RK3 steps)" > /dev/null
+python tools/ncu_summary.py $O/ncu_spx_wenoz.ncu-rep > $O/ncu_spx_wenoz_summary.txt 2>&1
 cp profiles/ncu_stage_summary_wenoz-rk3.json $O/
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_wenoz.csv \
+  $B --scheme wenoz-rk3 --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+python tools/launch_share.py $O/launches_wenoz.csv > $O/launch_share_wenoz.txt 2>&1
 
 # 3. launch list of the default bench command (cold-cache, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
