@@ -37,9 +37,14 @@ struct SpIdx {
   __device__ __forceinline__ int wy(int j) const {
     return j < 0 ? (by0 ? 0 : j + ny) : (j >= ny ? (by1 ? ny - 1 : j - ny) : j);
   }
-  // cell (i, j, k) of field f of a padded [z+gz][f][y][x] array (x, y resolved by the BCs)
-  __device__ __forceinline__ size_t at(int f, int i, int j, int k) const {
-    return (size_t)(k + gz) * ps + (size_t)f * fs + (size_t)wy(j) * nx + wx(i);
+  // field 0 of cell (i, j, k) of a padded [z+gz][f][y][x] array (x, y resolved by the BCs); the
+  // fields follow int(fs) apart.  The pointer is made opaque so
+  // that the field loads stay base + small offsets instead of a 64-bit index computation each
+  template <typename T>
+  __device__ __forceinline__ T* cell(T* base, int i, int j, int k) const {
+    T* p = base + ((size_t)(k + gz) * ps + (size_t)(wy(j) * nx + wx(i)));
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
   }
 };
 
@@ -76,14 +81,17 @@ __global__ void __launch_bounds__(256) k_sp_prim(SplitArgs a) {
     const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / X.fs) - 3;
     const bool interior = k >= 0 && k < a.nz;
     double u[NVS], v[NVS];
+    const double* pu = X.cell(a.Uin, i, j, k);
+    double* pv = X.cell(a.V, i, j, k);
+    const int fs = (int)X.fs;
 #pragma unroll
-    for (int f = 0; f < NVS; ++f) u[f] = __ldg(a.Uin + X.at(f, i, j, k));
+    for (int f = 0; f < NVS; ++f) u[f] = __ldg(pu + f * fs);
     if (interior && bad_state<NVS>(u))
       bad = min(bad, (unsigned long long)(((a.zoff + k) * a.ny + j) * (long long)a.nx + i));
     const bool fl = cons2prim<NVS>(u, v, a.c.gm1, a.c.p_floor);
     floors += (fl && interior) ? 1 : 0;
 #pragma unroll
-    for (int f = 0; f < NVS; ++f) a.V[X.at(f, i, j, k)] = v[f];
+    for (int f = 0; f < NVS; ++f) pv[f * fs] = v[f];
   }
   if (floors) atomicAdd(a.counters + 0, (unsigned long long)floors);
   if (bad != ULLONG_MAX) atomicMin(a.bad + a.stage, bad);
@@ -95,10 +103,13 @@ __device__ __forceinline__ bool sp_recon(const SplitArgs& a, const SpIdx& X, int
                                          double* qm) {
   constexpr int oi = D == 0, oj = D == 1, ok = D == 2;
   double c[5][NVS], p[NVS], m[NVS];
+  const int fs = (int)X.fs;
 #pragma unroll
-  for (int s = -2; s <= 2; ++s)
+  for (int s = -2; s <= 2; ++s) {
+    const double* v = X.cell(a.V, i + s * oi, j + s * oj, k + s * ok);
 #pragma unroll
-    for (int f = 0; f < NVS; ++f) c[s + 2][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
+    for (int f = 0; f < NVS; ++f) c[s + 2][f] = v[f * fs];
+  }
   const bool fb = weno_cell<NVS>(c[0], c[1], c[2], c[3], c[4], p, m);
   to_normal<NVS, D>(p, qp);
   to_normal<NVS, D>(m, qm);
@@ -112,9 +123,11 @@ __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* 
   double fn[NVS], fx[NVS];
   const int fell = face_flux<NVS, RS>(vl, vr, a.c, fn);
   from_normal<NVS, D>(fn, fx);
-  double* F = a.F[D];
+  double* F = a.F[D] + fidx(a, 0, i, j, k);
+  asm("mov.b64 %0, %0;" : "+l"(F));
+  const int fst = (a.ny + 1) * a.px;  // field stride of the flux arrays
 #pragma unroll
-  for (int f = 0; f < NVS; ++f) F[fidx(a, f, i, j, k)] = fx[f];
+  for (int f = 0; f < NVS; ++f) F[f * fst] = fx[f];
   return fell;
 }
 
@@ -202,19 +215,27 @@ __global__ void __launch_bounds__(256) k_sp_update(SplitArgs a) {
   const double* lam = a.c.lam;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(q % a.nx), j = (int)((q / a.nx) % a.ny), k = (int)(q / X.fs);
+    const int fs = (int)X.fs, fst = (a.ny + 1) * a.px, pl = NVS * fst;
+    const double* fx = a.F[0] + fidx(a, 0, i, j, k);
+    const double* fy = a.F[1] + fidx(a, 0, i, j, k);
+    const double* fz = a.F[2] + fidx(a, 0, i, j, k);
+    const double* pu = X.cell(a.Uin, i, j, k);
+    const double* pn = X.cell(a.Un, i, j, k);
+    double* po = X.cell(a.Uout, i, j, k);
+    double v[NVS];  // every load before the first store (Uout may alias U^n)
 #pragma unroll
     for (int f = 0; f < NVS; ++f) {
-      double r = lam[0] * (a.F[0][fidx(a, f, i + 1, j, k)] - a.F[0][fidx(a, f, i, j, k)]);
-      r = r + lam[1] * (a.F[1][fidx(a, f, i, j + 1, k)] - a.F[1][fidx(a, f, i, j, k)]);
-      r = r + lam[2] * (a.F[2][fidx(a, f, i, j, k + 1)] - a.F[2][fidx(a, f, i, j, k)]);
-      const size_t o = X.at(f, i, j, k);
-      const double s = __ldg(a.Uin + o) - r;
-      double v = s;
-      if (a.mode == 1) v = 0.5 * (a.Un[o] + s);                 // RK2: U^{n+1} = (U^n + U**)/2
-      else if (a.mode == 2) v = (a.wa * a.Un[o]) + (a.wb * s);  // RK3: (a U^n) + (b S(U))
-      if (f == NVS - 1 && a.last) v = v * a.c.damp;             // GLM damping once per step
-      a.Uout[o] = v;
+      double r = lam[0] * (__ldg(fx + f * fst + 1) - __ldg(fx + f * fst));
+      r = r + lam[1] * (__ldg(fy + f * fst + a.px) - __ldg(fy + f * fst));
+      r = r + lam[2] * (__ldg(fz + f * fst + pl) - __ldg(fz + f * fst));
+      const double s = __ldg(pu + f * fs) - r;
+      v[f] = s;
+      if (a.mode == 1) v[f] = 0.5 * (pn[f * fs] + s);                 // RK2: U^{n+1} = (U^n + U**)/2
+      else if (a.mode == 2) v[f] = (a.wa * pn[f * fs]) + (a.wb * s);  // RK3: (a U^n) + (b S(U))
     }
+    if (a.last) v[NVS - 1] = v[NVS - 1] * a.c.damp;  // GLM damping once per step
+#pragma unroll
+    for (int f = 0; f < NVS; ++f) po[f * fs] = v[f];
   }
 }
 
