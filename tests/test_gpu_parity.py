@@ -508,6 +508,18 @@ def test_cpa3d_full_period(mhd):
 # ---------------------------------------------------------------------------------------------
 # §8(f) row 2: SSP-RK3 (the paper's integrator), three state arrays
 # ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("limiter,stepper", [(I.MC, I.RK2), (I.WENOZ, I.RK3)])
+@pytest.mark.parametrize("bc", [(I.OUTFLOW, I.OUTFLOW, I.PERIODIC), (I.PERIODIC, I.OUTFLOW, I.OUTFLOW),
+                                (I.OUTFLOW, I.PERIODIC, I.OUTFLOW)])
+def test_mixed_boundaries_3d(mhd, limiter, stepper, bc):
+    """Outflow x / y (index clamp in the fused and split kernels) and z (ghost copies) on a
+    non-uniform ragged state (noisy OT-3D), against the oracle's materialised ghosts."""
+    p = I.orszag_tang_3d(32, limiter=limiter).replace(n=(40, 21, 19), hi=(1.25, 0.65625, 0.59375), bc=bc,
+                                                     stepper=stepper)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    assert_parity(*run_both(mhd, p, U0, 8))
+
+
 @pytest.mark.parametrize("case", ["ot3d", "brio_wu", "ot2d"])
 def test_rk3_parity(mhd, case):
     if case == "ot3d":
