@@ -70,6 +70,10 @@ def test_create_rejects_bad_arguments_without_gpu(lib):
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), C.byref(sc), None, C.byref(h)) == mhd.MHD_E_ARG
     d = mhd.Dist(0, 3, -1, 0)                # 3 ranks do not divide nz = 16
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), None, C.byref(d), C.byref(h)) == mhd.MHD_E_ARG
+    g4 = mhd.Grid()                          # nx * ny * 9 >= 2^31 (32-bit in-plane offsets)
+    for dd, n in enumerate((16384, 16384, 8)):
+        g4.n[dd], g4.lo[dd], g4.hi[dd] = n, 0.0, 1.0
+    assert lib.mhd_create(C.byref(g4), 5 / 3, 0.4, C.byref(bc), None, None, C.byref(h)) == mhd.MHD_E_ARG
     bc.lo[0] = 1                             # periodic on one side only
     assert lib.mhd_create(C.byref(g), 5 / 3, 0.4, C.byref(bc), None, None, C.byref(h)) == mhd.MHD_E_ARG
     assert h.value is None
