@@ -99,3 +99,22 @@ def test_halo_plan_shapes():
     assert mhd.halo_plan(1, 4, 64, True, 3)[0] == (2, 0, 16, 3) and mhd.halo_plan(1, 4, 64, True, 3)[3] == (2, 1, 19, 3)
     with pytest.raises(mhd.MhdError):
         mhd.halo_plan(0, 32, 64, True, 3)  # slab of 2 planes < ghost width 3
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """bench.py --impl reference launched the driver's way (torchrun, 2 ranks, 127.0.0.1): rank 0
+    alone prints one JSON line with impl "reference", the other rank exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "1", "--warmup", "0"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
