@@ -165,6 +165,17 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]);
 
+/* Device bytes of the context's state arrays (U^n, U*, U2 with RK3, the CT / split-stage
+ * scratch), each rounded up to 256 bytes: the size mhd_bind_workspace needs. */
+int mhd_workspace_bytes(mhd_ctx* ctx, size_t* bytes);
+
+/* Re-homes the context's state arrays into caller-owned device memory (e.g. a torch tensor from
+ * the caching allocator): dev_ptr on the context's device, 256-byte aligned, >= the
+ * mhd_workspace_bytes size.  The context frees the arrays it had allocated and only borrows
+ * these (mhd_destroy never frees them; the caller keeps them alive until then).  The state is
+ * cleared: call mhd_set_state next.  MHD_E_ARG on a short, misaligned or non-device buffer. */
+int mhd_bind_workspace(mhd_ctx* ctx, void* dev_ptr, size_t bytes);
+
 /* Pipelined host I/O (pinned host buffers, one full state each, caller-owned; the buffer must
  * stay valid and unmodified until mhd_io_join or the next call that waits on it):
  *  - mhd_set_state_async: starts the host->device copy of U ([nvar][z][y][x], as mhd_set_state)

@@ -47,6 +47,7 @@ struct mhd_ctx {
   double* spF[3] = {nullptr, nullptr, nullptr};   // split scratch: face fluxes over (nx+1)(ny+1)(nz+1)
   size_t spF_elems = 0;
   size_t arr_elems = 0;
+  bool borrowed = false;  // the state arrays live in caller memory (mhd_bind_workspace)
   unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..8] bad slots, [20] debug
   unsigned long long* dred = nullptr;  // reduction scratch for nranks > 1 (the first 9 entries)
   unsigned long long* hbuf = nullptr;  // pinned host mirror
@@ -719,6 +720,63 @@ int mhd_local_box(const mhd_ctx* c, int64_t off[3], int64_t ext[3]) {
   return MHD_OK;
 }
 
+// the state arrays of a context in workspace order, with their sizes in doubles
+struct WsArray {
+  double** p;
+  size_t n;
+};
+static int ws_arrays(mhd_ctx* c, WsArray out[10]) {
+  int k = 0;
+  out[k++] = {&c->U0, c->arr_elems};
+  out[k++] = {&c->U1, c->arr_elems};
+  if (c->scheme.stepper == MHD_RK3) out[k++] = {&c->U2, c->arr_elems};
+  if (c->scheme.ct || c->split) out[k++] = {&c->ctV, c->arr_elems};
+  for (int d = 0; d < 3; ++d) {
+    if (c->scheme.ct) out[k++] = {&c->ctF[d], c->arr_elems};
+    if (c->split) out[k++] = {&c->spF[d], c->spF_elems};
+  }
+  return k;
+}
+static size_t ws_round(size_t n) { return (n * sizeof(double) + 255) / 256 * 256; }
+
+int mhd_workspace_bytes(mhd_ctx* c, size_t* bytes) {
+  if (!c || !bytes) return MHD_E_ARG;
+  WsArray a[10];
+  const int n = ws_arrays(c, a);
+  size_t b = 0;
+  for (int i = 0; i < n; ++i) b += ws_round(a[i].n);
+  *bytes = b;
+  return MHD_OK;
+}
+
+int mhd_bind_workspace(mhd_ctx* c, void* dev_ptr, size_t bytes) {
+  if (!c || !dev_ptr) return MHD_E_ARG;
+  size_t need = 0;
+  mhd_workspace_bytes(c, &need);
+  if (bytes < need || ((uintptr_t)dev_ptr & 255)) return set_err(c, MHD_E_ARG, "workspace: %zu bytes, 256-byte aligned, needed", need);
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, dev_ptr) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device) {
+    cudaGetLastError();
+    return set_err(c, MHD_E_ARG, "workspace: not device memory of the context's device");
+  }
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  WsArray a[10];
+  const int n = ws_arrays(c, a);
+  char* p = static_cast<char*>(dev_ptr);
+  for (int i = 0; i < n; ++i) {
+    if (!c->borrowed && *a[i].p) cudaFree(*a[i].p);
+    *a[i].p = reinterpret_cast<double*>(p);
+    p += ws_round(a[i].n);
+  }
+  c->borrowed = true;
+  c->has_state = false;
+  c->in_pending = false;
+  c->ch_valid = false;
+  CUDA_OR_RETURN(c, cudaMemsetAsync(dev_ptr, 0, need, c->stream));  // ghost planes never hold garbage
+  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  return MHD_OK;
+}
+
 int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
   if (!c || !bytes) return MHD_E_ARG;
   *bytes = ((c->U2 ? 3 : 2) + (c->ctV ? (c->split ? 1 : 4) : 0)) * c->arr_elems * sizeof(double) +
@@ -1019,6 +1077,10 @@ const char* mhd_last_error(const mhd_ctx* c) { return c ? c->err : "null context
 
 void mhd_destroy(mhd_ctx* c) {
   if (!c) return;
+  if (c->borrowed) {  // caller-owned: forget, never free
+    c->U0 = c->U1 = c->U2 = c->ctV = nullptr;
+    for (int d = 0; d < 3; ++d) c->ctF[d] = c->spF[d] = nullptr;
+  }
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->h2d) cudaStreamSynchronize(c->h2d);
   if (c->d2h) cudaStreamSynchronize(c->d2h);

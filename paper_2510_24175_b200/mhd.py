@@ -29,7 +29,8 @@ EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_
            "mhd_set_state", "mhd_get_state", "mhd_compute_dt", "mhd_step", "mhd_get_diag", "mhd_last_error",
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
            "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
-           "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join")
+           "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join",
+           "mhd_workspace_bytes", "mhd_bind_workspace")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -88,6 +89,9 @@ def load() -> C.CDLL:
     L.mhd_get_state.argtypes = [P, P, C.c_int32]
     if hasattr(L, "mhd_get_state_box"):  # (absent from older builds used in A/B runs)
         L.mhd_get_state_box.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, C.c_int32]
+    if hasattr(L, "mhd_bind_workspace"):
+        L.mhd_workspace_bytes.argtypes = [P, C.POINTER(C.c_size_t)]
+        L.mhd_bind_workspace.argtypes = [P, P, C.c_size_t]
     if hasattr(L, "mhd_io_join"):
         L.mhd_set_state_async.argtypes = [P, P]
         L.mhd_get_state_async.argtypes = [P, P]
@@ -223,6 +227,18 @@ class Solver:
             raise ValueError(f"output must have shape {self.local_shape}")
         self._check(self._L.mhd_get_state(self._h, C.c_void_p(p), dev))
         return out
+
+    def workspace_bytes(self) -> int:
+        b = C.c_size_t()
+        self._check(self._L.mhd_workspace_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def bind_workspace(self, buf) -> None:
+        """Move the state arrays into a caller-owned CUDA tensor (>= workspace_bytes() bytes);
+        keep `buf` alive while the solver lives.  Clears the state."""
+        nbytes = buf.numel() * buf.element_size()
+        self._check(self._L.mhd_bind_workspace(self._h, C.c_void_p(buf.data_ptr()), nbytes))
+        self._workspace = buf
 
     def _host_ptr(self, U):
         p, dev, nbytes = _ptr_of(U)

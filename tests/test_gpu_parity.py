@@ -258,6 +258,37 @@ def test_state_roundtrip_host_and_device(mhd):
     s.destroy()
 
 
+@pytest.mark.parametrize("scheme", ["plm_rk2", "wenoz_rk3", "ct"])
+def test_bind_workspace_torch_memory(mhd, scheme):
+    """The state arrays re-homed into a torch-allocated CUDA buffer give the same run bitwise."""
+    import torch
+    from test_oracle_scheme import _random_ct_state
+    p = I.orszag_tang_3d(16).replace(n=(24, 20, 16))
+    if scheme == "wenoz_rk3":
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    if scheme == "ct":
+        p = p.replace(ct=1, glm=0)
+        U0 = _random_ct_state(p)
+    else:
+        U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    ref = mhd.Solver(p)
+    ref.set_state(U0)
+    log_r = ref.run(4)
+    want = ref.get_state()
+    ref.destroy()
+    s = mhd.Solver(p)
+    nb = s.workspace_bytes()
+    buf = torch.empty(nb + 256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(mhd.MhdError):
+        s.bind_workspace(buf[: nb - 256])  # too short
+    s.bind_workspace(buf)
+    s.set_state(U0)
+    log = s.run(4)
+    assert np.array_equal(log, log_r) and np.array_equal(s.get_state(), want)
+    s.destroy()
+    del buf
+
+
 def test_async_io_pipeline_equals_sync(mhd):
     """set_state_async / get_state_async / io_join (the pipelined e2e path) give the same dt
     sequence and states as the synchronous calls, step by step."""
