@@ -25,7 +25,10 @@
  *    mhd_get_state / mhd_get_diag / mhd_last_error / mhd_destroy returns MHD_E_STATE until
  *    the next successful mhd_set_state.
  *  - Collective semantics: with nranks > 1, mhd_create, mhd_compute_dt, mhd_step and
- *    mhd_destroy must be called by every rank in the same order (as with NCCL).
+ *    mhd_destroy must be called by every rank in the same order (as with NCCL).  A
+ *    synchronising call that sees neither progress nor an NCCL error for MHD_NCCL_TIMEOUT_S
+ *    seconds (environment, default 600) aborts the communicator and returns the sticky
+ *    MHD_E_NCCL (a neighbour rank that died or stopped calling).
  *  - A context is not thread-safe; different contexts are independent.
  */
 #ifndef MHD_H

@@ -13,8 +13,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/mhd.h"
@@ -111,6 +113,39 @@ int set_err(mhd_ctx* c, int code, const char* fmt, ...) {
   } while (0)
 
 size_t plane_elems(const mhd_ctx* c) { return (size_t)c->nv * c->nx * c->ny; }
+
+// Host wait for the context's stream.  With NCCL slabs the stream may wait on collectives of
+// the other ranks: poll it together with ncclCommGetAsyncError and give up after
+// MHD_NCCL_TIMEOUT_S seconds (default 600): the communicator is aborted and the context gets
+// the sticky MHD_E_NCCL (a rank that died or stopped calling would otherwise hang every
+// synchronising call; SPEC.md:106's neighbour timeout).
+int sync_stream(mhd_ctx* c) {
+  if (!(c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL && c->comm)) {
+    CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+    return MHD_OK;
+  }
+  double limit = 600.0;
+  if (const char* e = getenv("MHD_NCCL_TIMEOUT_S")) limit = atof(e) > 0.0 ? atof(e) : limit;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long spins = 0;; ++spins) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return MHD_OK;
+    if (q != cudaErrorNotReady) return set_err(c, MHD_E_CUDA, "stream: %s", cudaGetErrorString(q));
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return set_err(c, MHD_E_NCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ae));
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return set_err(c, MHD_E_NCCL, "NCCL timeout: no progress for %.0f s (a neighbour rank stopped?)", limit);
+    }
+    if (spins < 2000) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
 
 int check_sticky(mhd_ctx* c) {
   if (c->sticky != MHD_OK)
@@ -432,7 +467,7 @@ int reduce_and_read(mhd_ctx* c) {
     src = c->dred;
   }
   CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf, src, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (int rs = sync_stream(c)) return rs;
   c->diag.p_floors = (int64_t)c->hbuf[2];
   c->diag.plm_fallbacks = (int64_t)c->hbuf[3];
   c->diag.hlld_to_hll = (int64_t)c->hbuf[4];
@@ -809,7 +844,7 @@ int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "validate: %s", cudaGetErrorString(e));
   CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf + 5, c->dbuf + 5, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                     c->stream));
-  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (int rs = sync_stream(c)) return rs;
   if (c->hbuf[5] != ~0ULL) {
     c->diag.bad_stage = 0;
     c->diag.first_bad_cell = (int64_t)c->hbuf[5];
@@ -833,7 +868,7 @@ int mhd_get_state(mhd_ctx* c, double* U, int32_t on_device) {
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "unpack: %s", cudaGetErrorString(e));
   if (!on_device)
     CUDA_OR_RETURN(c, cudaMemcpyAsync(U, c->U1, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (int rs = sync_stream(c)) return rs;
   return MHD_OK;
 }
 
@@ -895,7 +930,7 @@ int mhd_get_state_box(mhd_ctx* c, const int64_t off[3], const int64_t ext[3], do
       CUDA_OR_RETURN(c, cudaMemcpy2DAsync(dst, (size_t)ext[0] * sizeof(double), src, (size_t)c->nx * sizeof(double),
                                           (size_t)ext[0] * sizeof(double), (size_t)ext[1], kind, c->stream));
     }
-  CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
+  if (int rs = sync_stream(c)) return rs;
   return MHD_OK;
 }
 
