@@ -23,6 +23,7 @@
 // --fmad=false so that results equal the CPU oracle bitwise.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
@@ -588,34 +589,37 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
 template <int DIM, int NV>
 __global__ void __launch_bounds__(256) k_dt(DtArgs a) {
   const int nx = a.nx, ny = a.ny, nzl = a.nz_loc;
-  const size_t fstride = (size_t)nx * ny, pstride = fstride * NV;
-  const size_t ncell = fstride * nzl;
+  const int fs = nx * ny;  // (mhd_create bounds nx*ny*9 below 2^31)
+  const size_t pstride = (size_t)fs * NV;
   double M = 0.0, Sx = 0.0;
   unsigned long long badidx = ULLONG_MAX;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ncell; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t k = i / fstride, cell = i % fstride;
-    double u[NV], v[NV];
-    load_cell<NV>(a.U, (k + a.gz) * pstride, fstride, cell, u);
-    if (bad_state<NV>(u)) {
-      badidx = min(badidx, (unsigned long long)((a.zoff + k) * fstride + cell));
-      continue;
-    }
-    cons2prim<NV>(u, v, a.gm1, a.p_floor);
-    double inv = 0.0, smax = 0.0;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      const double cf = fast_speed(a.gamma, v[0], v[4], v[5 + d], v[5 + (d + 1) % 3], v[5 + (d + 2) % 3]);
-      const double s = fabs(v[1 + d]) + cf;
-      if (d == 0) {
-        inv = s * a.idx[0];
-        smax = s;
-      } else {
-        inv = inv + s * a.idx[d];
-        smax = fmax(smax, s);
+  // planes over blockIdx.y, cells of a plane over x: 32-bit in-plane indices, no 64-bit division
+  for (int k = blockIdx.y; k < nzl; k += gridDim.y) {
+    const double* plane = a.U + (size_t)(k + a.gz) * pstride;
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < fs; cell += gridDim.x * blockDim.x) {
+      double u[NV], v[NV];
+      load_fields<NV>(plane + cell, fs, u);
+      if (bad_state<NV>(u)) {
+        badidx = min(badidx, (unsigned long long)((a.zoff + k) * (long long)fs + cell));
+        continue;
       }
+      cons2prim<NV>(u, v, a.gm1, a.p_floor);
+      double inv = 0.0, smax = 0.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        const double cf = fast_speed(a.gamma, v[0], v[4], v[5 + d], v[5 + (d + 1) % 3], v[5 + (d + 2) % 3]);
+        const double s = fabs(v[1 + d]) + cf;
+        if (d == 0) {
+          inv = s * a.idx[0];
+          smax = s;
+        } else {
+          inv = inv + s * a.idx[d];
+          smax = fmax(smax, s);
+        }
+      }
+      M = fmax(M, inv);
+      Sx = fmax(Sx, smax);
     }
-    M = fmax(M, inv);
-    Sx = fmax(Sx, smax);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -807,15 +811,15 @@ int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter) {
 }
 
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st) {
-  const size_t ncell = (size_t)a.nx * a.ny * a.nz_loc;
-  size_t blocks = (ncell + 255) / 256;
-  const size_t cap = (size_t)nsm * 8;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  if (dim == 3) k_dt<3, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else if (dim == 2) k_dt<2, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else if (nv == 9) k_dt<1, 9><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else k_dt<1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  // ~8 blocks of 256 per SM in total: x covers a plane (capped), y strides over the planes
+  const size_t fs = (size_t)a.nx * a.ny, cap = (size_t)nsm * 8;
+  const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>((fs + 255) / 256, cap));
+  const unsigned by = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)a.nz_loc, cap / bx));
+  const dim3 g(bx, by);
+  if (dim == 3) k_dt<3, 9><<<g, 256, 0, st>>>(a);
+  else if (dim == 2) k_dt<2, 9><<<g, 256, 0, st>>>(a);
+  else if (nv == 9) k_dt<1, 9><<<g, 256, 0, st>>>(a);
+  else k_dt<1, 8><<<g, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
