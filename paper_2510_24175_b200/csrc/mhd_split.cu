@@ -132,10 +132,13 @@ __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* 
 }
 
 constexpr int kSpSeg = 16;  // faces per marching segment (at most; segments of a line are balanced)
+#ifndef MHD_SP_MINB
+#define MHD_SP_MINB 3  // 3 blocks of 128 per SM (<= 168 registers): +2% over no bound, 4 spills more
+#endif
 
 // y and z faces: lane = x (coalesced), a thread marches one 16-face segment of a line
 template <int D, int RS>
-__global__ void __launch_bounds__(128) k_sp_face_m(SplitArgs a) {
+__global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_m(SplitArgs a) {
   const SpIdx X = make_idx(a);
   const int nb = D == 1 ? a.nz : a.ny;         // second line coordinate: k (y lines) or j (z lines)
   const int nm = D == 1 ? a.ny + 1 : a.nz + 1;  // faces per line
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(128) k_sp_face_m(SplitArgs a) {
 // x faces i in [0, nx] of the rows (j, k): warps over the 32-cell chunks of [0, nx), q+ of cell
 // i-1 from lane l-1; the faces at chunk starts and the last face nx in a second pass, one per thread
 template <int RS>
-__global__ void __launch_bounds__(128) k_sp_face_x(SplitArgs a) {
+__global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_x(SplitArgs a) {
   const SpIdx X = make_idx(a);
   const int nf = a.nx, nch = (nf + 31) / 32;
   const size_t items = (size_t)nch * a.ny * a.nz;
