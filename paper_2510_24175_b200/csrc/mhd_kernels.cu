@@ -735,18 +735,12 @@ template <int DIM, int NV, int RS, int TY, int REC>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
   using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
   auto kern = k_stage<DIM, NV, RS, TY, REC>;
-  static bool attr_set = false;
-  static size_t extra = 0;  // MHD_EXTRA_SMEM (bytes): measurement knob for the L1 carve-out
-  if (!attr_set) {
-    const char* e_ = getenv("MHD_EXTRA_SMEM");
-    extra = e_ ? (size_t)atol(e_) : 0;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(S::bytes + extra));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // (the attribute is per device: set on every launch, a host-side call of ~1 us)
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  if (e != cudaSuccess) return e;
   if (a.ze <= a.zb) return cudaSuccess;
   dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.ze - a.zb + a.kz - 1) / a.kz);
-  kern<<<grid, S::NT, S::bytes + extra, st>>>(a);
+  kern<<<grid, S::NT, S::bytes, st>>>(a);
   return cudaGetLastError();
 }
 
