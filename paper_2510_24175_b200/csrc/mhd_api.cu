@@ -466,7 +466,9 @@ int reduce_and_read(mhd_ctx* c) {
     NCCL_OR_RETURN(c, ncclGroupEnd());
     src = c->dred;
   }
-  CUDA_OR_RETURN(c, cudaMemcpyAsync(c->hbuf, src, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  // (a kernel store into the mapped pinned buffer, not a copy-engine transfer: see k_store_words)
+  cudaError_t es = mhd::launch_store_words(c->hbuf, src, 9, c->stream);
+  if (es != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt read-back: %s", cudaGetErrorString(es));
   if (int rs = sync_stream(c)) return rs;
   c->diag.p_floors = (int64_t)c->hbuf[2];
   c->diag.plm_fallbacks = (int64_t)c->hbuf[3];

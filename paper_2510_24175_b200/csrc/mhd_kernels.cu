@@ -704,6 +704,18 @@ __global__ void k_face_flux(const double* __restrict__ VL, const double* __restr
   if (cnt) atomicAdd(nhll, (unsigned long long)cnt);
 }
 
+// n words of device memory into pinned (mapped) host memory by a kernel instead of a copy-engine
+// transfer: the per-step dt read-back is not queued behind a large asynchronous device->host
+// state copy on the same engine (mhd_get_state_async)
+__global__ void k_store_words(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_store_words(unsigned long long* host_dst, const unsigned long long* src, int n, cudaStream_t st) {
+  k_store_words<<<1, 32, 0, st>>>(host_dst, src, n);
+  return cudaGetLastError();
+}
+
 // test-only: the branch-free operator sequences next to the IEEE operators (mhd_device.cuh)
 __global__ void k_fast_ops(const double* __restrict__ A, const double* __restrict__ B, long long n,
                            double* __restrict__ out, int* __restrict__ okm) {

@@ -88,6 +88,7 @@ cudaError_t launch_pack(const double* src, double* dst, int nv, int nx, int ny, 
                         int nsm, cudaStream_t st);
 cudaError_t launch_validate(const double* U, int nv, int nx, int ny, int nzl, int gz, long long zoff, double gm1,
                             unsigned long long* bad, int nsm, cudaStream_t st, int check_p);
+cudaError_t launch_store_words(unsigned long long* host_dst, const unsigned long long* src, int n, cudaStream_t st);
 cudaError_t launch_fast_ops(const double* A, const double* B, long long n, double* out, int* okm, cudaStream_t st);
 cudaError_t launch_face_flux(int nv, int riemann, const double* VL, const double* VR, long long n,
                              const StageConsts& c, double* F, unsigned long long* nhll, cudaStream_t st);
