@@ -240,14 +240,16 @@ __global__ void __launch_bounds__(256) k_ct_update(CtArgs a) {
     s[5] = __ldg(a.Uin + X.at(5, i, j, k)) - rbx;
     s[6] = __ldg(a.Uin + X.at(6, i, j, k)) - rby;
     s[7] = __ldg(a.Uin + X.at(7, i, j, k)) - rbz;
+    double v[8];  // every U^n load before the first store (Uout may alias U^n)
 #pragma unroll
     for (int f = 0; f < 8; ++f) {
       const size_t o = X.at(f, i, j, k);
-      double v = s[f];
-      if (a.mode == 1) v = 0.5 * (a.Un[o] + s[f]);
-      else if (a.mode == 2) v = (a.wa * a.Un[o]) + (a.wb * s[f]);
-      a.Uout[o] = v;
+      v[f] = s[f];
+      if (a.mode == 1) v[f] = 0.5 * (a.Un[o] + s[f]);
+      else if (a.mode == 2) v[f] = (a.wa * a.Un[o]) + (a.wb * s[f]);
     }
+#pragma unroll
+    for (int f = 0; f < 8; ++f) a.Uout[X.at(f, i, j, k)] = v[f];
   }
 }
 
