@@ -203,6 +203,13 @@ int mhd_io_join(mhd_ctx* ctx);
  * too large to copy out whole.) */
 int mhd_get_state_box(mhd_ctx* ctx, const int64_t off[3], const int64_t ext[3], double* U, int32_t on_device);
 
+/* The driver loop in native code (R26 / the oracle's orc_run): up to nsteps of
+ * { dt = mhd_compute_dt; with t_end > 0 the step that would pass t_end takes dt = t_end - t;
+ * mhd_step(dt); t = t + dt } while t < t_end (t_end <= 0: no end time).  dt_log (host, may be
+ * NULL) receives the dts (capacity nsteps), *done the steps taken.  Collective with nranks > 1.
+ * Returns the status of the first failing call (the steps before it stay done). */
+int mhd_run(mhd_ctx* ctx, int64_t nsteps, double t_end, double* dt_log, int64_t* done);
+
 /* Counters and the unphysical-state record.  On one GPU the counters are read back from the
  * device (synchronising) and include every completed step; with NCCL slabs they are the global
  * sums reduced by the last mhd_compute_dt (the collective). */

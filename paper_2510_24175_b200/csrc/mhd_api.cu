@@ -1009,6 +1009,24 @@ int mhd_step(mhd_ctx* c, double dt) {
   return MHD_OK;
 }
 
+int mhd_run(mhd_ctx* c, int64_t nsteps, double t_end, double* dt_log, int64_t* done) {
+  if (!c || nsteps < 0 || !std::isfinite(t_end)) return MHD_E_ARG;
+  int64_t n = 0;
+  double t = 0.0;
+  int rc = MHD_OK;
+  while (n < nsteps && (t_end <= 0.0 || t < t_end)) {
+    double dt = 0.0;
+    if ((rc = mhd_compute_dt(c, &dt))) break;
+    if (t_end > 0.0 && t + dt > t_end) dt = t_end - t;  // the last step lands on t_end
+    if ((rc = mhd_step(c, dt))) break;
+    if (dt_log) dt_log[n] = dt;
+    ++n;
+    t = t + dt;
+  }
+  if (done) *done = n;
+  return rc;
+}
+
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]) {
   if (!plan) return MHD_E_ARG;

@@ -30,7 +30,7 @@ EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
            "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
            "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join",
-           "mhd_workspace_bytes", "mhd_bind_workspace")
+           "mhd_workspace_bytes", "mhd_bind_workspace", "mhd_run")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -89,6 +89,8 @@ def load() -> C.CDLL:
     L.mhd_get_state.argtypes = [P, P, C.c_int32]
     if hasattr(L, "mhd_get_state_box"):  # (absent from older builds used in A/B runs)
         L.mhd_get_state_box.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, C.c_int32]
+    if hasattr(L, "mhd_run"):
+        L.mhd_run.argtypes = [P, C.c_int64, C.c_double, P, C.POINTER(C.c_int64)]
     if hasattr(L, "mhd_bind_workspace"):
         L.mhd_workspace_bytes.argtypes = [P, C.POINTER(C.c_size_t)]
         L.mhd_bind_workspace.argtypes = [P, P, C.c_size_t]
@@ -315,17 +317,12 @@ class Solver:
 
     # --- harness (DESIGN.md §3 c.14 driver loop) ---------------------------------------------
     def run(self, nsteps: int, t_end: float = 0.0):
-        """compute_dt/step loop; with t_end > 0 the last dt is clamped.  Returns the dt log."""
-        log = []
-        t = 0.0
-        while len(log) < nsteps and (t_end <= 0.0 or t < t_end):
-            dt = self.compute_dt()
-            if t_end > 0.0 and t + dt > t_end:
-                dt = t_end - t
-            self.step(dt)
-            log.append(dt)
-            t = t + dt
-        return np.array(log, dtype=np.float64)
+        """mhd_run: the compute_dt/step loop in native code; with t_end > 0 the last dt is
+        clamped.  Returns the dt log."""
+        log = np.zeros(max(int(nsteps), 1), dtype=np.float64)
+        done = C.c_int64()
+        self._check(self._L.mhd_run(self._h, int(nsteps), float(t_end), C.c_void_p(log.ctypes.data), C.byref(done)))
+        return log[:done.value].copy()
 
 
 class SolverGroup:
