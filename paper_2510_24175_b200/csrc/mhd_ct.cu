@@ -94,7 +94,7 @@ __device__ __forceinline__ bool ct_recon(const CtArgs& a, const CtIdx& X, int i,
   for (int s = -H; s <= H; ++s)
 #pragma unroll
     for (int f = 0; f < 8; ++f) c[s + H][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
-  if constexpr (REC == 2) return weno_cell<8>(c[0], c[1], c[2], c[3], c[4], qp, qm);
+  if constexpr (REC == 2) return weno_cell<8, true>(c[0], c[1], c[2], c[3], c[4], qp, qm);
   else return plm_cell<8, REC>(c[0], c[1], c[2], qp, qm);
 }
 
