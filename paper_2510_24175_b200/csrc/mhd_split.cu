@@ -110,7 +110,10 @@ __device__ __forceinline__ bool sp_recon(const SplitArgs& a, const SpIdx& X, int
 #pragma unroll
     for (int f = 0; f < NVS; ++f) c[s + 2][f] = v[f * fs];
   }
-  const bool fb = weno_cell<NVS>(c[0], c[1], c[2], c[3], c[4], p, m);
+#ifndef MHD_SP_INL
+#define MHD_SP_INL 1  // bit D: inline WENO-Z in the D-face kernel (x only: -2%; y, z slower inlined)
+#endif
+  const bool fb = weno_cell<NVS, (MHD_SP_INL >> D) & 1>(c[0], c[1], c[2], c[3], c[4], p, m);
   to_normal<NVS, D>(p, qp);
   to_normal<NVS, D>(m, qm);
   return fb;
