@@ -2,22 +2,25 @@
 //
 // Rows of SURVEY.md §8(a) → kernels:
 //   a1 ghost fill   : x/y periodic/outflow resolved by index wrap/clamp inside the stage
-//                     kernel (no ghost columns exist); z ghost planes (2 per side) are filled
-//                     by copies (1 GPU) or NCCL send/recv (slabs) in mhd_api.cu.
-//   a2..a5          : k_stage — one fused kernel per RK stage: cons->prim, PLM, GLM
-//                     pre-solve + HLL/HLLD face fluxes in x/y/z, flux divergence, stage
-//                     update (stage 2: RK2 average in place over U^n and psi damping).
+//                     kernel (no ghost columns exist); z ghost planes (2 per side, 3 for
+//                     WENO-Z) are filled by copies (1 GPU) or NCCL send/recv (slabs) in mhd_api.cu.
+//   a2..a5          : k_stage — one fused kernel per RK stage: cons->prim, PLM (or WENO-Z in
+//                     1D/2D), GLM pre-solve + HLL/HLLD face fluxes in x/y/z, flux divergence,
+//                     the RK epilogue (RK2 average / RK3 weights) and psi damping.  (3D WENO-Z
+//                     runs the split stage of mhd_split.cu; CT the stage of mhd_ct.cu.)
 //   a6              : k_dt — CFL dt / c_h partial maxima (warp shuffle -> block -> int64
 //                     atomicMax on non-negative doubles, exact and order-free).
 //
-// k_stage design: a CTA owns a 32 x TY column tile and marches over a chunk
-// of z planes.  Lane = x (coalesced 256 B rows per field), warp = y row.  Shared memory
-// holds the primitive plane k with a 2-cell x/y halo (for the x and y faces), the
-// primitive plane k+1 (for the z slope of k+1), and per column the PLM state V+(k) and
-// the z-face flux F(k-1/2) carried to the next plane, plus the y-face fluxes of plane k.
-// x-face fluxes never touch shared memory: lane i computes face i-1/2 and takes face
-// i+1/2 from lane i+1 by __shfl_down_sync (lane 31 reads the tile's extra face from smem).
-// Every face is solved once per stage except the faces on tile edges in x and y (3%..5%).
+// k_stage design: a CTA owns a 32 x TY column tile (TY cell warps + one edge
+// warp) and marches over a chunk of z planes.  Lane = x (coalesced 256 B rows per field),
+// warp = y row.  Shared memory holds the primitive plane k with a G-cell x/y halo (Vc), per
+// column V+(k) in the z normal frame (Vpz) and the z fluxes of faces k-1/2, k+1/2 (Fz
+// ping-pong), the y- and x-face fluxes of plane k (Fy, Fx), and q+ of the cells left of the
+// tile (XP).  Each cell is reconstructed once along z (V+ carried) and along x (q+ passed to
+// the next lane by shuffle); along y both cells of a face are reconstructed.  Every face is
+// solved once per stage except the faces on tile edges in x and y (3%..5%), through one
+// inlined, branch-free face solve (a face whose division / sqrt range tests fail is re-solved
+// out of line with the IEEE operators, exact_face).
 //
 // All arithmetic is the recipe of DESIGN.md §3 (see mhd_device.cuh), built with
 // --fmad=false so that results equal the CPU oracle bitwise.
