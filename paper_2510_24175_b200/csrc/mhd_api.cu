@@ -1,11 +1,15 @@
 // mhd_api.cu — host side of libmhd: the C ABI declared in include/mhd.h.
 //
-// Owns the device state (two padded fp64 arrays, U^n and U*), the stream, the z-slab plan
-// and the NCCL communicator; sequences one SSP-RK2 step as
-//   [z ghost planes of U^n] -> k_stage(stage 1) -> [z ghost planes of U*] -> k_stage(stage 2)
+// Owns the device state (padded fp64 arrays U^n, U* [, U2 for RK3] and the CT / split-stage
+// scratch; or borrowed from the caller, mhd_bind_workspace), the streams, the z-slab plan and
+// the NCCL communicator; sequences one RK step as, per stage,
+//   [z ghost planes of the stage input: copies / NCCL halo] -> stage kernel(s)
 // (§3.2: boundary exchange, then the offloaded per-cell/per-face work, per
-// Runge-Kutta stage; the boundary exchange is the only inter-GPU step), and
-// the CFL reduction as k_dt -> ncclAllReduce(max) -> 16-byte read-back.
+// Runge-Kutta stage; the boundary exchange is the only inter-GPU step), with the
+// fused k_stage overlapping the halo with its interior planes; and the CFL reduction as
+// k_dt -> ncclAllReduce(max) -> a 72-byte kernel store into mapped host memory.
+// Also: pipelined host I/O (async set/get state), the native driver loop (mhd_run), the
+// in-process slab group (decomposition tests on one GPU) and kernel timing.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
