@@ -91,7 +91,7 @@ struct mhd_ctx {
 
 namespace {
 
-const char* kVersion = "libmhd sm_100a fused-stage-v1 (fp64, --fmad=false)";
+const char* kVersion = "libmhd sm_100a fused-stage-v2, split WENO-Z and CT stages (fp64, --fmad=false)";
 
 int set_err(mhd_ctx* c, int code, const char* fmt, ...) {
   if (c) {
