@@ -358,8 +358,9 @@ def main():
                          f"{args.n}^3 {args.workload} IC, {el:.1f} s on {cores} OpenMP threads"}
 
     s.destroy()
-    # kernels per RK stage: the fused k_stage, or five launches for CT and for the 3D GLM WENO-Z
-    # split stage (mhd_split.cu; MHD_FUSED_WENOZ=1 selects the fused kernel); plus k_dt per step
+    # kernels per step: k_dt + the dt read-back store, and per RK stage the fused k_stage, or five
+    # launches for CT and for the 3D GLM WENO-Z
+    # split stage (mhd_split.cu; MHD_FUSED_WENOZ=1 selects the fused kernel)
     split = (p.limiter == I.WENOZ and p.n[2] > 1 and not p.ct and os.environ.get("MHD_FUSED_WENOZ") != "1")
     launches_per_stage = 5 if (p.ct or split) else 1
     if rank == 0:
@@ -369,7 +370,7 @@ def main():
                 "config": {"workload": f"{args.workload}_{args.n}^3_per_gpu ({WORKLOADS[args.workload]}; global {p.n[0]}x{p.n[1]}x{p.n[2]})",
                            "scheme": SCHEMES[args.scheme], "cells": cells,
                            "parallelism": f"z-slab x{world}", "l2": "inputs larger than L2 (2 x 1.27 GB arrays per GPU)"},
-                "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * (1 + (3 if p.stepper else 2) * launches_per_stage),
+                "roofline": roof, "clocks": clk.summary(), "gpu_launches": args.steps * (2 + (3 if p.stepper else 2) * launches_per_stage),
                 "e2e": e2e, "cpu_baseline": cpu, "diag": diag,
                 "lib": mhd.version()}
         print(json.dumps(line), flush=True)
