@@ -3,6 +3,7 @@ identical seeded inputs.  Bar (BASELINE.json north star): per-field relative L-i
 exactly equal dt sequence; the recipe is designed for bitwise equality, so the
 tests also report/require equal counters.  Sizes span several 32 x 8 tiles and ragged tails."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -401,7 +402,7 @@ def test_ot3d_256_full_size_parity(mhd):
     assert_parity(*res)
 
 
-def _sampled_step_parity(mhd, workload, p, samples, halo=4):
+def _sampled_step_parity(mhd, workload, p, samples, halo=4, box_bc=None):
     """One step of a full-size BASELINE config on the GPU, in bench.py's launch configuration,
     checked on sampled cells: the dt equals the oracle's on the whole state (bitwise), and each
     sampled cell equals the oracle's step of its (2*halo+1)^3 neighbourhood (the PLM-RK2 update
@@ -416,8 +417,8 @@ def _sampled_step_parity(mhd, workload, p, samples, halo=4):
     s.step(dt_g)
     w = 2 * halo + 1
     dx = [(p.hi[d] - p.lo[d]) / p.n[d] for d in range(3)]
-    sub = p.replace(n=(w, w, w), lo=(0.0, 0.0, 0.0), hi=(w * dx[0], w * dx[1], w * dx[2]),
-                    bc=(I.OUTFLOW, I.OUTFLOW, I.OUTFLOW))
+    bc = box_bc if box_bc is not None else I.OUTFLOW
+    sub = p.replace(n=(w, w, w), lo=(0.0, 0.0, 0.0), hi=(w * dx[0], w * dx[1], w * dx[2]), bc=(bc, bc, bc))
     assert all((sub.hi[d] - sub.lo[d]) / w == dx[d] for d in range(3))  # identical dt/dx
     for (x, y, z) in samples:
         ix = [(x + o) % p.n[0] for o in range(-halo, halo + 1)]
@@ -452,6 +453,23 @@ def test_blast_512_full_size_sampled(mhd):
         v = 0.5 + (0.1 + rng.uniform(-3, 3) / 512) * v / np.linalg.norm(v)
         front.append(tuple(int(np.clip(c * 512, 0, 511)) for c in v))
     _sampled_step_parity(mhd, "blast3d", p, _edge_and_random_cells(p.n, 16, rng, front))
+
+
+@pytest.mark.parametrize("scheme", ["wenoz-rk3", "ct-wenoz-rk3"])
+def test_paper_schemes_256_full_size_sampled(mhd, scheme):
+    """The §8(f) bench lines at their full size (OT-3D 256^3, bench.py --scheme): one step of
+    WENO-Z + HLLD + RK3 with GLM (the split stage) or with CT, on sampled cells.  An RK3 step of a
+    WENO-Z cell reads +-9 cells; the oracle box is 21^3 (outflow for GLM; periodic for CT, whose
+    wrap seam reaches at most 9 cells in by the third stage, short of the centre)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    p = bench.build_problem("ot3d", 1, 256, scheme)
+    rng = np.random.default_rng(21)
+    _sampled_step_parity(mhd, "ot3d", p, _edge_and_random_cells(p.n, 12, rng), halo=10,
+                         box_bc=I.PERIODIC if p.ct else I.OUTFLOW)
 
 
 @pytest.mark.slow
