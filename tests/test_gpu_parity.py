@@ -455,10 +455,11 @@ def test_blast_512_full_size_sampled(mhd):
     _sampled_step_parity(mhd, "blast3d", p, _edge_and_random_cells(p.n, 16, rng, front))
 
 
-@pytest.mark.parametrize("scheme", ["wenoz-rk3", "ct-wenoz-rk3"])
-def test_paper_schemes_256_full_size_sampled(mhd, scheme):
-    """The §8(f) bench lines at their full size (OT-3D 256^3, bench.py --scheme): one step of
-    WENO-Z + HLLD + RK3 with GLM (the split stage) or with CT, on sampled cells.  An RK3 step of a
+@pytest.mark.parametrize("workload,scheme", [("ot3d", "wenoz-rk3"), ("ot3d", "ct-wenoz-rk3"), ("cpa3d", "plm-rk2")])
+def test_paper_schemes_256_full_size_sampled(mhd, workload, scheme):
+    """The §8(f) bench lines at their full size (256^3, bench.py --workload / --scheme): one step of
+    WENO-Z + HLLD + RK3 with GLM (the split stage) or with CT, and the 3D CPA workload, on sampled
+    cells.  An RK3 step of a
     WENO-Z cell reads +-9 cells; the oracle box is 21^3 (outflow for GLM; periodic for CT, whose
     wrap seam reaches at most 9 cells in by the third stage, short of the centre)."""
     import importlib.util
@@ -466,9 +467,9 @@ def test_paper_schemes_256_full_size_sampled(mhd, scheme):
         os.path.abspath(__file__))), "bench.py"))
     bench = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(bench)
-    p = bench.build_problem("ot3d", 1, 256, scheme)
+    p = bench.build_problem(workload, 1, 256, scheme)
     rng = np.random.default_rng(21)
-    _sampled_step_parity(mhd, "ot3d", p, _edge_and_random_cells(p.n, 12, rng), halo=10,
+    _sampled_step_parity(mhd, workload, p, _edge_and_random_cells(p.n, 12, rng), halo=10 if p.limiter == I.WENOZ else 4,
                          box_bc=I.PERIODIC if p.ct else I.OUTFLOW)
 
 
