@@ -290,6 +290,34 @@ def test_bind_workspace_torch_memory(mhd, scheme):
     del buf
 
 
+@pytest.mark.parametrize("limiter", [I.MC, I.WENOZ])
+def test_z_chunking_and_repeat_invariance(mhd, limiter):
+    """The result does not depend on the z chunk length of the stage kernel's CTAs (each chunk
+    re-derives its prologue: V+(kb-1), the first z face) nor on the run: kz = 1, 3, 7 and the
+    model's choice, twice, all bitwise equal (the fused kernel in 2-plane-chunk corner cases)."""
+    p = I.orszag_tang_3d(24, limiter=limiter).replace(n=(40, 21, 19), hi=(1.25, 0.65625, 0.59375))
+    if limiter == I.WENOZ:  # the fused kernel (3D WENO-Z defaults to the split stage)
+        os.environ["MHD_FUSED_WENOZ"] = "1"
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    outs = []
+    try:
+        for kz in ("1", "3", "7", "", ""):
+            if kz:
+                os.environ["MHD_KZ"] = kz
+            else:
+                os.environ.pop("MHD_KZ", None)
+            s = mhd.Solver(p)
+            s.set_state(U0)
+            log = s.run(4)
+            outs.append((log, s.get_state()))
+            s.destroy()
+    finally:
+        os.environ.pop("MHD_KZ", None)
+        os.environ.pop("MHD_FUSED_WENOZ", None)
+    for log, U in outs[1:]:
+        assert np.array_equal(log, outs[0][0]) and np.array_equal(U, outs[0][1])
+
+
 def test_async_io_pipeline_equals_sync(mhd):
     """set_state_async / get_state_async / io_join (the pipelined e2e path) give the same dt
     sequence and states as the synchronous calls, step by step."""
