@@ -290,6 +290,59 @@ def test_bind_workspace_torch_memory(mhd, scheme):
     del buf
 
 
+def _harsh_state(limiter, seed, p_lo, vmax, rho_lo):
+    """Random cells (log-uniform density and pressure, uniform velocity and field): pressure
+    floors, reconstruction fallbacks and HLLD -> HLL fallbacks all occur."""
+    p = I.orszag_tang_3d(32, limiter=limiter).replace(n=(32, 24, 20), hi=(1.0, 0.75, 0.625))
+    rng = np.random.default_rng(seed)
+    sh = (p.n[2], p.n[1], p.n[0])
+    rho = 10.0 ** rng.uniform(rho_lo, 1, sh)
+    pr = 10.0 ** rng.uniform(p_lo, -2, sh)
+    v = rng.uniform(-vmax, vmax, (3,) + sh)
+    B = rng.uniform(-2, 2, (3,) + sh)
+    return p, I.prim_to_cons_ic(p, rho, v[0], v[1], v[2], pr, B[0], B[1], B[2])
+
+
+@pytest.mark.parametrize("case", ["plm_rk2", "wenoz_rk3_split", "wenoz_rk3_fused"])
+def test_rare_event_counters_parity(mhd, case):
+    """The rare events the owner-rule counters record (pressure floors, reconstruction
+    positivity fallbacks, HLLD -> HLL fallbacks) occur, and the GPU counts equal the oracle's."""
+    if case == "plm_rk2":
+        p, U0 = _harsh_state(I.MC, 0, -13, 3.0, -2)
+        n, need = 3, ("p_floors", "hlld_to_hll")  # (PLM is positivity preserving here)
+    else:
+        p, U0 = _harsh_state(I.WENOZ, 0, -13, 0.3, -1)
+        p = p.replace(stepper=I.RK3)
+        n, need = 2, ("p_floors", "plm_fallbacks", "hlld_to_hll")
+    if case == "wenoz_rk3_fused":
+        os.environ["MHD_FUSED_WENOZ"] = "1"
+    try:
+        res = run_both(mhd, p, U0, n)
+    finally:
+        os.environ.pop("MHD_FUSED_WENOZ", None)
+    assert_parity(*res)
+    co = res[0].counters()
+    assert all(co[k] > 0 for k in need), co
+
+
+def test_unphysical_detection_matches_oracle(mhd):
+    """A run that turns unphysical: the GPU reports the same first bad cell and stage as the
+    oracle (lowest global linear index, atomicMin)."""
+    p, U0 = _harsh_state(I.WENOZ, 0, -13, 3.0, -2)
+    p = p.replace(stepper=I.RK3)
+    o = oracle.Oracle(p, U0)
+    with pytest.raises(oracle.OracleError) as ei:
+        o.run(3)
+    want = ei.value.counters.as_dict()
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    with pytest.raises(mhd.MhdError):
+        s.run(3)
+    d = s.diag()
+    s.destroy()
+    assert (d["first_bad_cell"], d["bad_stage"]) == (want["first_bad_cell"], want["bad_stage"]), (d, want)
+
+
 @pytest.mark.parametrize("limiter", [I.MC, I.WENOZ])
 def test_z_chunking_and_repeat_invariance(mhd, limiter):
     """The result does not depend on the z chunk length of the stage kernel's CTAs (each chunk
