@@ -325,6 +325,31 @@ def test_rare_event_counters_parity(mhd, case):
     assert all(co[k] > 0 for k in need), co
 
 
+@pytest.mark.parametrize("limiter,P", [(I.MC, 2), (I.MC, 4), (I.WENOZ, 2), (I.WENOZ, 4)])
+def test_rare_event_counters_slab_group(mhd, limiter, P):
+    """Owner rule across slab boundaries: with rare events on every slab, P slabs count exactly
+    what one domain counts (and produce the same bits)."""
+    if limiter == I.MC:
+        p, U0 = _harsh_state(I.MC, 1, -13, 3.0, -2)
+    else:
+        p, U0 = _harsh_state(I.WENOZ, 1, -13, 0.3, -1)
+        p = p.replace(stepper=I.RK3)
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    log1 = s.run(2)
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    g = mhd.SolverGroup(p, P)
+    g.set_state(U0)
+    logP = g.run(2)
+    UP, dP = g.get_state(), g.diag()
+    g.destroy()
+    assert np.array_equal(log1, logP) and np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k], (k, d1[k], dP[k])
+    assert d1["p_floors"] > 0 and d1["hlld_to_hll"] > 0
+
+
 def test_unphysical_detection_matches_oracle(mhd):
     """A run that turns unphysical: the GPU reports the same first bad cell and stage as the
     oracle (lowest global linear index, atomicMin)."""
