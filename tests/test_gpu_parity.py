@@ -383,6 +383,46 @@ def test_smallest_grids(mhd, scheme, n):
     assert_parity(*run_both(mhd, p, U0, 5))
 
 
+def _random_config(seed):
+    """A seeded random problem: dimension and limiter cycle with the seed; extents (ragged,
+    >= 4), boundary conditions per axis, Riemann solver, stepper, GLM or CT and a smooth random
+    state with noise are drawn."""
+    rng = np.random.default_rng(1000 + seed)
+    dim = 1 + seed % 3
+    limiter = (I.MINMOD, I.MC, I.WENOZ)[(seed // 3) % 3]
+    n = [int(rng.integers(4, 41)) if d < dim else 1 for d in range(3)]
+    ct = dim == 3 and (seed // 9) % 2 == 1
+    bc = tuple(int(rng.integers(0, 2)) if (d < dim and not ct) else I.PERIODIC for d in range(3))
+    glm = 1 if (dim >= 2 and not ct) else int(rng.integers(0, 2)) if not ct else 0
+    p = I.Problem("rnd", tuple(n), hi=tuple(n[d] / 32 if d < dim else 1.0 for d in range(3)), bc=bc,
+                  gamma=float(rng.choice([5 / 3, 1.4, 2.0])), limiter=limiter, riemann=int(rng.integers(0, 2)),
+                  glm=glm, stepper=int(rng.integers(0, 2)), ct=int(ct))
+    X, Y, Z = I.mesh(p)
+    k = rng.uniform(1, 3, 3) * 2 * math.pi
+    ph = rng.uniform(0, 2 * math.pi, 8)
+    w = lambda j: np.sin(k[0] * X + ph[j]) * np.cos(k[1] * Y + ph[j]) * np.cos(k[2] * Z + 0.5 * ph[j])
+    rho = 1.0 + 0.4 * w(0)
+    pr = 0.6 + 0.3 * w(1)
+    v = [0.5 * w(2), 0.5 * w(3), 0.5 * w(4) if dim == 3 else 0.0 * w(4)]
+    B = [0.6 + 0.3 * w(5), 0.4 * w(6), 0.4 * w(7)]
+    if dim == 1:
+        B[0] = 0.75 + 0.0 * X  # constant normal field in 1D
+    U0 = I.prim_to_cons_ic(p, rho, v[0], v[1], v[2], pr, B[0], B[1], B[2])
+    if ct:
+        from test_oracle_scheme import _random_ct_state
+        U0 = _random_ct_state(p)
+    return p, I.with_noise(U0, p, amp=1e-3, seed=int(rng.integers(1 << 30))) if not ct else U0
+
+
+@pytest.mark.parametrize("seed", range(18))
+def test_random_configurations(mhd, seed):
+    """Seeded random problems across every option the ABI takes (dimension, ragged extents,
+    per-axis periodic / outflow, minmod / MC / WENO-Z, HLL / HLLD, RK2 / RK3, GLM on / off in
+    1D, CT in 3D): the GPU equals the oracle bitwise."""
+    p, U0 = _random_config(seed)
+    assert_parity(*run_both(mhd, p, np.ascontiguousarray(U0), 6))
+
+
 @pytest.mark.parametrize("limiter", [I.MC, I.WENOZ])
 def test_z_chunking_and_repeat_invariance(mhd, limiter):
     """The result does not depend on the z chunk length of the stage kernel's CTAs (each chunk
