@@ -423,6 +423,30 @@ def test_random_configurations(mhd, seed):
     assert_parity(*run_both(mhd, p, np.ascontiguousarray(U0), 6))
 
 
+@pytest.mark.parametrize("seed", [2, 5, 8, 11, 14])
+def test_random_configurations_slab_group(mhd, seed):
+    """The 3D random configurations split into P in-process z slabs (P the largest of 2..5 that
+    divides nz with slabs at least the ghost depth): bitwise equal to one domain, equal counters."""
+    p, U0 = _random_config(seed)
+    gz = (3 if p.limiter == I.WENOZ else 2) + (1 if p.ct else 0)
+    Ps = [P for P in (5, 4, 3, 2) if p.n[2] % P == 0 and p.n[2] // P >= gz]
+    if not Ps:
+        pytest.skip(f"nz = {p.n[2]} has no admissible slab count")
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    log1 = s.run(4)
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    g = mhd.SolverGroup(p, Ps[0])
+    g.set_state(np.ascontiguousarray(U0))
+    logP = g.run(4)
+    UP, dP = g.get_state(), g.diag()
+    g.destroy()
+    assert np.array_equal(log1, logP) and np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k], (k, d1[k], dP[k])
+
+
 @pytest.mark.parametrize("limiter", [I.MC, I.WENOZ])
 def test_z_chunking_and_repeat_invariance(mhd, limiter):
     """The result does not depend on the z chunk length of the stage kernel's CTAs (each chunk
