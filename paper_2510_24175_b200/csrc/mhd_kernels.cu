@@ -537,10 +537,17 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       __syncthreads();
       continue;
     }
-    // ---- update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads of U
-    // and U^n follow the barrier (held across it they would spill; both planes were prefetched
-    // into L1 at the top of the iteration).
+    // ---- advance the plane window (3D) and update.  After this barrier every read of Vc (the
+    // face jobs) is done, so plane k+1 is loaded first: its conversions' L2 latency overlaps the
+    // update, which reads only the flux buffers.  The next barrier publishes the window and
+    // orders this update before the next plane's flux writes.
+    // Update: S(U) = U - r, r = lx dFx (+ ly dFy) (+ lz dFz).  The pointwise loads of U and U^n
+    // follow the barrier (held across it they would spill; both planes were prefetched into L1
+    // at the top of the iteration).
     __syncthreads();
+    if constexpr (DIM == 3) {
+      if (k + 1 < ke) load_plane(k + 1, false);
+    }
     if (own) {  // (own: the cell is not wrapped, own_cell = gy * nx + gx)
       const size_t off = (size_t)a.gz * pstride + own_cell;
       const double* pu = opaque(at(a.Uin + off, k));
@@ -567,14 +574,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         po[f * fs] = v;
       }
     }
-    // ---- advance the plane window (3D).  No barrier before the load: the update reads only
-    // the flux buffers, and every read of Vc (the face jobs) finished at the barrier above;
-    // the barrier after it also orders this update before the next plane's flux writes.
     if constexpr (DIM == 3) {
-      if (k + 1 < ke) {
-        load_plane(k + 1, false);
-        __syncthreads();
-      }
+      if (k + 1 < ke) __syncthreads();
     }
   }
   __syncthreads();
