@@ -359,10 +359,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
     if (DIM == 3 && cellw) {
-      // latency hiding: own column of plane k+3 (first touched next iteration) into L2; own
-      // cell of planes k+1, k+2 (the z job) and of plane k (update; U^n in stage 2) into L1
-      const double* p2 = opaque(at(Ucol, k + G + 1 < nzl + a.gz ? k + G + 1 : k));
-      const double* p1 = opaque(at(Ucol, k + G));
+      // latency hiding, one iteration ahead: the own cell of plane k+G+1 (the z job's newest
+      // plane next iteration) into L1 and of plane k+G+2 into L2; U^n of plane k (the update,
+      // stage 2) into L1
+      const double* p2 = opaque(at(Ucol, k + G + 2 < nzl + a.gz ? k + G + 2 : k));
+      const double* p1 = opaque(at(Ucol, k + G + 1 < nzl + a.gz ? k + G + 1 : k));
       const double* pn = opaque(at(a.Un + (size_t)a.gz * pstride + own_cell, k));
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
