@@ -15,12 +15,13 @@
  *  - extern "C", fp64 only; every call returns an int status (MHD_OK = 0); nothing throws.
  *  - Layout at the ABI: U[f][z][y][x], x fastest, this rank's interior cells only,
  *    nvar = 8 + (glm != 0) fields in the order (rho, mx, my, mz, E, Bx, By, Bz, psi).
- *    Internally the library keeps padded [z][f][y][x] arrays with 2 ghost cells per side
- *    on every active axis.
+ *    Internally the library keeps padded [z][f][y][x] arrays with g ghost planes at each z
+ *    end (g = 2 PLM, 3 WENO-Z, one more with CT) and no x/y ghost columns.
  *  - Ownership: the caller owns every host or device buffer it passes; the context owns
  *    the device state it allocates and its NCCL communicator.
  *  - Asynchrony: mhd_step is asynchronous with respect to the host (it enqueues on the
- *    context's stream); mhd_compute_dt and mhd_get_state synchronise.
+ *    context's stream); mhd_compute_dt, mhd_set_state, mhd_get_state and mhd_get_state_box
+ *    synchronise; the *_async calls and mhd_io_join do not.
  *  - Errors are sticky: after MHD_E_UNPHYSICAL, MHD_E_CUDA or MHD_E_NCCL every call except
  *    mhd_get_state / mhd_get_diag / mhd_last_error / mhd_destroy returns MHD_E_STATE until
  *    the next successful mhd_set_state.
@@ -115,9 +116,9 @@ typedef struct mhd_ctx mhd_ctx; /* opaque; created by mhd_create, freed by mhd_d
 /* rank 0 only; 128 bytes to broadcast to the other ranks before mhd_create. */
 int mhd_nccl_get_unique_id(uint8_t out[128]);
 
-/* Validates the arguments (MHD_E_ARG), plans the slab, allocates the two padded state
- * arrays (U^n and U*; a third with MHD_RK3) on the device and, for nranks > 1, creates the NCCL communicator
- * (collective).  gamma > 1, 0 < cfl < 1, each active extent >= 4, nx * ny * 9 < 2^31 (32-bit
+/* Validates the arguments (MHD_E_ARG), plans the slab, allocates the padded state arrays
+ * (U^n and U*; a third with MHD_RK3; the scratch of the CT and 3D WENO-Z stages) on the device
+ * and, for nranks > 1, creates the NCCL communicator (collective).  gamma > 1, 0 < cfl < 1, each active extent >= 4, nx * ny * 9 < 2^31 (32-bit
  * offsets within a z plane).  *out receives the context (NULL on failure). */
 int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
                const mhd_scheme* scheme, const mhd_dist* dist, mhd_ctx** out);
@@ -129,7 +130,8 @@ int mhd_set_stream(mhd_ctx* ctx, void* cuda_stream);
 /* This rank's interior block in global cell coordinates. */
 int mhd_local_box(const mhd_ctx* ctx, int64_t off[3], int64_t ext[3]);
 
-/* Bytes of device memory the context holds. */
+/* Bytes of device memory the context's state arrays and records take (the lazily allocated
+ * async-I/O staging arrays excluded). */
 int mhd_device_bytes(const mhd_ctx* ctx, size_t* bytes);
 
 /* Copy a state in: U is [nvar][ext_z][ext_y][ext_x] (mhd_local_box), host memory when
@@ -144,7 +146,7 @@ int mhd_get_state(mhd_ctx* ctx, double* U, int32_t on_device);
 /* CFL dt of the current state (row a6): dt = cfl / max_cells sum_d
  * (|v_d| + c_f,d)/dx_d, global over ranks (collective); also caches c_h = max_cells
  * max_d (|v_d| + c_f,d) for the next mhd_step.  Reports an unphysical state found by the
- * preceding mhd_step.  Host-synchronising (16-byte read-back). */
+ * preceding mhd_step.  Host-synchronising (a 72-byte record stored into mapped host memory). */
 int mhd_compute_dt(mhd_ctx* ctx, double* dt);
 
 /* One SSP-RK2 (or RK3) step (rows a1-a5) with the given dt > 0 and the c_h cached
@@ -164,7 +166,7 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt);
 /* Halo plan of a z slab (pure host logic, no GPU): the 4 transfers of one RK stage in posting
  * order, each as (peer rank or -1, 0 = send / 1 = recv, first storage plane, plane count);
  * storage planes are 0..nz_loc+2*ghost-1 with `ghost` ghost planes at each end (2 for PLM,
- * 3 for WENOZ).  Returns MHD_E_ARG on inconsistent arguments. */
+ * 3 for WENOZ, one more with CT).  Returns MHD_E_ARG on inconsistent arguments. */
 int mhd_halo_plan(int32_t rank, int32_t nranks, int64_t nz_glob, int32_t z_periodic, int32_t ghost,
                   int32_t plan[4][4]);
 
