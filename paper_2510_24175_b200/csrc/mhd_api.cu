@@ -52,6 +52,8 @@ struct mhd_ctx {
   bool split = false;                             // 3D GLM WENO-Z: the five-launch stage (mhd_split.cu)
   double* spF[3] = {nullptr, nullptr, nullptr};   // split scratch: face fluxes over (nx+1)(ny+1)(nz+1)
   size_t spF_elems = 0;
+  cudaStream_t sp_aux[2] = {nullptr, nullptr};  // split stage: the y and z face kernels' streams
+  cudaEvent_t sp_ev[3] = {nullptr, nullptr, nullptr};
   size_t arr_elems = 0;
   bool borrowed = false;  // the state arrays live in caller memory (mhd_bind_workspace)
   unsigned long long* dbuf = nullptr;  // [0,1] dt maxima bits, [2..4] counters, [5..8] bad slots, [20] debug
@@ -433,7 +435,11 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.bad = c->dbuf + 5;
   if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
   const int pr = prof_begin(c, 0);
-  cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream);
+  if (!c->sp_aux[0]) {  // (the y and z face kernels run on two auxiliary streams: -1%)
+    for (int i = 0; i < 2; ++i) CUDA_OR_RETURN(c, cudaStreamCreateWithFlags(&c->sp_aux[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) CUDA_OR_RETURN(c, cudaEventCreateWithFlags(&c->sp_ev[i], cudaEventDisableTiming));
+  }
+  cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "split stage %d: %s", stage, cudaGetErrorString(e));
   return MHD_OK;
@@ -1141,6 +1147,13 @@ void mhd_destroy(mhd_ctx* c) {
     for (int d = 0; d < 3; ++d) c->ctF[d] = c->spF[d] = nullptr;
   }
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int i = 0; i < 2; ++i)
+    if (c->sp_aux[i]) {
+      cudaStreamSynchronize(c->sp_aux[i]);
+      cudaStreamDestroy(c->sp_aux[i]);
+    }
+  for (int i = 0; i < 3; ++i)
+    if (c->sp_ev[i]) cudaEventDestroy(c->sp_ev[i]);
   if (c->h2d) cudaStreamSynchronize(c->h2d);
   if (c->d2h) cudaStreamSynchronize(c->d2h);
   if (c->io_in) cudaFree(c->io_in);

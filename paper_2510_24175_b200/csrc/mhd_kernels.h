@@ -78,7 +78,8 @@ struct SplitArgs {
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
   unsigned long long* bad;       // [4] per stage
 };
-cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st);
+cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
+                               cudaStream_t aux2, cudaEvent_t* ev);
 inline int split_row_pitch(int nx) { return (nx + 1 + 31) / 32 * 32; }
 cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st);
 int stage_tile_rows(int dim, int limiter);

@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(256) k_sp_update(SplitArgs a) {
   }
 }
 
-cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st) {
+cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
+                               cudaStream_t aux2, cudaEvent_t* ev) {
   const size_t pc = (size_t)a.nx * a.ny;
   auto grid = [&](size_t n, int bs, int per_sm) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((n + bs - 1) / bs, (size_t)nsm * per_sm));
@@ -254,14 +255,28 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
   const size_t segz = (size_t)a.nx * a.ny * ((a.nz + 1 + kSpSeg - 1) / kSpSeg);
   const size_t xw = (size_t)((a.nx + 31) / 32) * 32 * a.ny * a.nz;
   k_sp_prim<<<grid(pc * (a.nz + 6), 256, 16), 256, 0, st>>>(a);
+  // the three face kernels are independent (V in, their own F out): y and z on two auxiliary
+  // streams, joined before the update, so one kernel's tail overlaps the others
+  cudaStream_t s1 = aux1 ? aux1 : st, s2 = aux2 ? aux2 : st;
+  if (aux1) {
+    cudaEventRecord(ev[0], st);
+    cudaStreamWaitEvent(s1, ev[0], 0);
+    cudaStreamWaitEvent(s2, ev[0], 0);
+  }
   if (riemann) {
     k_sp_face_x<1><<<grid(xw, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<1, 1><<<grid(segy, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<2, 1><<<grid(segz, 128, 32), 128, 0, st>>>(a);
+    k_sp_face_m<1, 1><<<grid(segy, 128, 32), 128, 0, s1>>>(a);
+    k_sp_face_m<2, 1><<<grid(segz, 128, 32), 128, 0, s2>>>(a);
   } else {
     k_sp_face_x<0><<<grid(xw, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<1, 0><<<grid(segy, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<2, 0><<<grid(segz, 128, 32), 128, 0, st>>>(a);
+    k_sp_face_m<1, 0><<<grid(segy, 128, 32), 128, 0, s1>>>(a);
+    k_sp_face_m<2, 0><<<grid(segz, 128, 32), 128, 0, s2>>>(a);
+  }
+  if (aux1) {
+    cudaEventRecord(ev[1], s1);
+    cudaEventRecord(ev[2], s2);
+    cudaStreamWaitEvent(st, ev[1], 0);
+    cudaStreamWaitEvent(st, ev[2], 0);
   }
   k_sp_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
   return cudaGetLastError();
