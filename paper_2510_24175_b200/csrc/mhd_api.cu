@@ -375,6 +375,15 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   return MHD_OK;
 }
 
+// the two auxiliary streams (and fork/join events) on which the split and CT stages run their
+// y and z face kernels next to the x one (-1%)
+int aux_streams(mhd_ctx* c) {
+  if (c->sp_aux[0]) return MHD_OK;
+  for (int i = 0; i < 2; ++i) CUDA_OR_RETURN(c, cudaStreamCreateWithFlags(&c->sp_aux[i], cudaStreamNonBlocking));
+  for (int i = 0; i < 3; ++i) CUDA_OR_RETURN(c, cudaEventCreateWithFlags(&c->sp_ev[i], cudaEventDisableTiming));
+  return MHD_OK;
+}
+
 // one CT stage (mhd_ct.cu): prim, three face passes, update with the RK epilogue
 int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   const StagePlan sp = stage_plan(c, stage);
@@ -399,7 +408,8 @@ int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
   const int pr = prof_begin(c, 0);
-  cudaError_t e = mhd::launch_ct_stage(c->scheme.riemann, a, c->nsm, c->stream);
+  if (int rc_aux = aux_streams(c)) return rc_aux;
+  cudaError_t e = mhd::launch_ct_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "ct stage %d: %s", stage, cudaGetErrorString(e));
   return MHD_OK;
@@ -435,10 +445,7 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.bad = c->dbuf + 5;
   if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
   const int pr = prof_begin(c, 0);
-  if (!c->sp_aux[0]) {  // (the y and z face kernels run on two auxiliary streams: -1%)
-    for (int i = 0; i < 2; ++i) CUDA_OR_RETURN(c, cudaStreamCreateWithFlags(&c->sp_aux[i], cudaStreamNonBlocking));
-    for (int i = 0; i < 3; ++i) CUDA_OR_RETURN(c, cudaEventCreateWithFlags(&c->sp_ev[i], cudaEventDisableTiming));
-  }
+  if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "split stage %d: %s", stage, cudaGetErrorString(e));

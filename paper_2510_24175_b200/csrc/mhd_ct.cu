@@ -254,31 +254,47 @@ __global__ void __launch_bounds__(256) k_ct_update(CtArgs a) {
 }
 
 template <int RS, int REC>
-static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st) {
+static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1, cudaStream_t aux2,
+                               cudaEvent_t* ev) {
   const size_t pc = (size_t)a.nx * a.ny;
   auto grid = [&](size_t n, int bs, int per_sm) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((n + bs - 1) / bs, (size_t)nsm * per_sm));
   };
   k_ct_prim<<<grid(pc * (a.nz + 2 * a.G), 256, 16), 256, 0, st>>>(a);
+  // the three face kernels are independent: y and z on two auxiliary streams, joined before
+  // the update
+  cudaStream_t s1 = aux1 ? aux1 : st, s2 = aux2 ? aux2 : st;
+  if (aux1) {
+    cudaEventRecord(ev[0], st);
+    cudaStreamWaitEvent(s1, ev[0], 0);
+    cudaStreamWaitEvent(s2, ev[0], 0);
+  }
   k_ct_face_x<RS, REC><<<grid((size_t)((a.nx + 31) / 32) * 32 * a.ny * (a.nz + 2), 128, 32), 128, 0, st>>>(a);
   const size_t segy = (size_t)a.nx * (a.nz + 2) * ((a.ny + kCtSeg - 1) / kCtSeg);
   const size_t segz = (size_t)a.nx * a.ny * ((a.nz + 1 + kCtSeg - 1) / kCtSeg);
-  k_ct_face_m<1, RS, REC><<<grid(segy, 128, 32), 128, 0, st>>>(a);
-  k_ct_face_m<2, RS, REC><<<grid(segz, 128, 32), 128, 0, st>>>(a);
+  k_ct_face_m<1, RS, REC><<<grid(segy, 128, 32), 128, 0, s1>>>(a);
+  k_ct_face_m<2, RS, REC><<<grid(segz, 128, 32), 128, 0, s2>>>(a);
+  if (aux1) {
+    cudaEventRecord(ev[1], s1);
+    cudaEventRecord(ev[2], s2);
+    cudaStreamWaitEvent(st, ev[1], 0);
+    cudaStreamWaitEvent(st, ev[2], 0);
+  }
   k_ct_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st) {
+cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
+                            cudaStream_t aux2, cudaEvent_t* ev) {
   const int lim = a.c.limiter;
   if (riemann) {
-    if (lim == 2) return launch_ct_t<1, 2>(a, nsm, st);
-    if (lim == 1) return launch_ct_t<1, 1>(a, nsm, st);
-    return launch_ct_t<1, 0>(a, nsm, st);
+    if (lim == 2) return launch_ct_t<1, 2>(a, nsm, st, aux1, aux2, ev);
+    if (lim == 1) return launch_ct_t<1, 1>(a, nsm, st, aux1, aux2, ev);
+    return launch_ct_t<1, 0>(a, nsm, st, aux1, aux2, ev);
   }
-  if (lim == 2) return launch_ct_t<0, 2>(a, nsm, st);
-  if (lim == 1) return launch_ct_t<0, 1>(a, nsm, st);
-  return launch_ct_t<0, 0>(a, nsm, st);
+  if (lim == 2) return launch_ct_t<0, 2>(a, nsm, st, aux1, aux2, ev);
+  if (lim == 1) return launch_ct_t<0, 1>(a, nsm, st, aux1, aux2, ev);
+  return launch_ct_t<0, 0>(a, nsm, st, aux1, aux2, ev);
 }
 
 // dt / c_h maxima with the face-averaged B (3.12 with R32)

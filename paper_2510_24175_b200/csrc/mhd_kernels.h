@@ -58,7 +58,8 @@ struct CtArgs {
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
   unsigned long long* bad;       // [4] per stage
 };
-cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st);
+cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
+                            cudaStream_t aux2, cudaEvent_t* ev);
 
 // the WENO-Z stage of the 3D GLM path as five launches (mhd_split.cu)
 constexpr int NVS = 9;
