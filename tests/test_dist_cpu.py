@@ -118,3 +118,52 @@ def test_reference_arm_under_torchrun_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _simulate_plans(world, nz_glob, periodic, ghost):
+    """Execute every rank's halo plan with NCCL's pairing rule (the k-th send from a to b meets
+    the k-th receive on b from a) on numpy slabs; return the slabs and the global array."""
+    from paper_2510_24175_b200 import mhd
+    rng = np.random.default_rng(world * 100 + nz_glob + ghost)
+    G = rng.standard_normal((nz_glob, 3, 2, 2))
+    nz = nz_glob // world
+    S = []
+    for r in range(world):
+        s = np.full((nz + 2 * ghost, 3, 2, 2), np.nan)
+        s[ghost:ghost + nz] = G[r * nz:(r + 1) * nz]
+        S.append(s)
+    sends, recvs = {}, {}
+    for r in range(world):
+        for peer, kind, first, count in mhd.halo_plan(r, world, nz_glob, periodic, ghost):
+            if peer < 0:
+                continue
+            key = (r, peer) if kind == 0 else (peer, r)
+            (sends if kind == 0 else recvs).setdefault(key, []).append((r, first, count))
+    assert sends.keys() == recvs.keys()
+    for key in sends:
+        assert len(sends[key]) == len(recvs[key]), key
+        for (src, f0, c0), (dst, f1, c1) in zip(sends[key], recvs[key]):
+            assert c0 == c1
+            S[dst][f1:f1 + c1] = S[src][f0:f0 + c0]
+    return S, G, nz
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("ghost", [2, 3, 4])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_halo_plan_all_rank_counts(world, ghost, periodic):
+    """Up to the 8 ranks of one node, every ghost depth the stages use (2 PLM, 3 WENO-Z, 4 CT with
+    WENO-Z): executing all plans together fills every ghost plane with the global neighbour plane
+    (periodic wrap) or leaves it to the local outflow copy at the domain ends."""
+    from paper_2510_24175_b200 import build
+    build.build()
+    nz_glob = world * max(ghost, 4)
+    S, G, nz = _simulate_plans(world, nz_glob, periodic, ghost)
+    for r in range(world):
+        z0 = r * nz
+        for m in range(ghost):
+            for sp, zg in ((m, z0 - ghost + m), (nz + ghost + m, z0 + nz + m)):
+                if world > 1 and (periodic or 0 <= zg < nz_glob):
+                    assert np.array_equal(S[r][sp], G[zg % nz_glob]), (r, sp, zg)
+                elif world > 1:
+                    assert np.isnan(S[r][sp]).all()
