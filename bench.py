@@ -60,14 +60,49 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks, power and clock-event (throttle) reasons during the timed region
+    (B200_PROFILING.md's clocks line).  NVML polled every 20 ms from a thread (the timed region is
+    ~0.1 s, shorter than nvidia-smi's start-up), one sample taken on entry and one on exit;
+    falls back to `nvidia-smi -lms 200` without NVML."""
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.rows = []  # (sm_mhz, max_mhz, power_w, {reasons})
         self.proc = None
+        self.nv = None
+        self.stop = threading.Event()
+
+    def _nvml_sample(self):
+        nv, h = self.nv, self.h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        masks = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        self.rows.append((float(sm), float(mx), pw, {n for n, m in zip(self.NAMES, masks) if bits & m}))
+
+    def _nvml_loop(self):
+        while not self.stop.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nv = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -75,21 +110,30 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._smi_read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
         time.sleep(0.3)
         return self
 
-    def _read(self):
+    def _smi_read(self):
         for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                num = lambda x: float(x) if x.replace(".", "").isdigit() else None
+                self.rows.append((num(p[0]), num(p[1]), num(p[2]),
+                                  {n for i, n in enumerate(self.NAMES) if p[3 + i].lower() == "active"}))
 
     def __exit__(self, *exc):
-        if self.proc is not None:
+        if self.nv is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+        elif self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
             try:
@@ -100,13 +144,13 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [r[0] for r in self.rows if r[0] is not None]
+        mx = [r[1] for r in self.rows if r[1] is not None]
+        pw = [r[2] for r in self.rows if r[2] is not None]
+        reasons = sorted(set().union(*(r[3] for r in self.rows)))
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None,
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 SCHEMES = {
