@@ -1192,6 +1192,11 @@ int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
   if (!c) return MHD_E_ARG;
   if (c->prof) prof_drain(c);
   c->prof = enable != 0;
+  while (c->prof && c->ev_pool.size() < 256) {  // created up front: none inside a timed loop
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    c->ev_pool.push_back(e);
+  }
   c->prof_ms[0] = c->prof_ms[1] = 0.0;
   c->prof_n[0] = c->prof_n[1] = 0;
   return MHD_OK;
