@@ -626,6 +626,29 @@ def _edge_and_random_cells(n, k, rng, extra=()):
     return cells + list(extra)
 
 
+def test_long_run_conservation_ot3d(mhd):
+    """A long GPU run (OT-3D 128^3, 400 steps, into the turbulent phase) keeps the periodic
+    invariants the scheme has at any size: total mass, momentum, energy and magnetic field
+    conserved to round-off, and the GLM-controlled divergence of B stays small."""
+    p = I.orszag_tang_3d(128)
+    U0 = I.orszag_tang_3d_ic(p)
+    s = mhd.Solver(p)
+    s.set_state(np.ascontiguousarray(U0))
+    log = s.run(400)
+    U = s.get_state()
+    d = s.diag()
+    s.destroy()
+    assert len(log) == 400 and np.all(np.isfinite(U)) and d["first_bad_cell"] == -1
+    for f in range(8):  # (B_z starts at zero: scale by the final field as well)
+        scale = max(np.abs(U0[f]).sum(), np.abs(U[f]).sum())
+        assert abs(U[f].sum() - U0[f].sum()) <= 1e-11 * scale, f
+    dx = 1.0 / 128
+    bx, by, bz = U[5], U[6], U[7]
+    div = ((np.roll(bx, -1, 2) - np.roll(bx, 1, 2)) + (np.roll(by, -1, 1) - np.roll(by, 1, 1)) +
+           (np.roll(bz, -1, 0) - np.roll(bz, 1, 0))) / (2 * dx)
+    assert np.sqrt((div * dx) ** 2).mean() / np.sqrt((bx * bx + by * by + bz * bz).mean()) < 0.05
+
+
 @pytest.mark.slow
 def test_blast_512_full_size_sampled(mhd):
     """BASELINE configs[3] per GPU (blast 512^3, one rank's slab): one step, sampled cells,
