@@ -304,7 +304,8 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region (device time, CUDA events on the library's stream = torch's current stream)
-    s.profile_enable(True)
+    nst = 3 if p.stepper else 2
+    s.profile_enable(True, capacity=args.steps * (nst + 1) + 8)  # one event pair per stage and per dt pass
     with ClockSampler(local_rank) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -406,7 +407,8 @@ def main():
     # launches for CT and for the 3D GLM WENO-Z
     # split stage (mhd_split.cu; MHD_FUSED_WENOZ=1 selects the fused kernel)
     split = (p.limiter == I.WENOZ and p.n[2] > 1 and not p.ct and os.environ.get("MHD_FUSED_WENOZ") != "1")
-    launches_per_stage = 5 if (p.ct or split) else 1
+    # with slabs the fused stage is three launches (interior, then the two boundary ranges)
+    launches_per_stage = 5 if (p.ct or split) else (3 if world > 1 else 1)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

@@ -230,11 +230,16 @@ void mhd_destroy(mhd_ctx* ctx);
 int mhd_debug_face_flux(mhd_ctx* ctx, const double* VL, const double* VR, int64_t n, double ch,
                         double* F, int64_t* n_hll);
 
-/* Kernel timing (measurement support for bench.py): while enabled, every
- * launch of the fused stage kernel and of the dt kernel is bracketed by CUDA events on the
- * context's stream.  mhd_profile_read synchronises, adds up the event intervals recorded
- * since enable, and returns total milliseconds and launch counts per kernel class
- * (index 0: stage kernel, 1: dt kernel).  Enabling resets the totals. */
+/* Kernel timing (measurement support for bench.py): while enabled, every RK
+ * stage (class 0: all its launches — the fused kernel, or with slabs its interior launch, the
+ * wait for the halo and its two boundary launches; the five launches of a split WENO-Z or CT
+ * stage) and every dt pass (class 1: the dt kernel) is bracketed by one pair of CUDA events on
+ * the context's stream.  enable: 0 off; 1 on with room for 1024 pairs; n > 1 on with room for n
+ * pairs.  The events are created here, so none is created and nothing synchronises inside a
+ * timed loop; units beyond the capacity are not recorded and make mhd_profile_read return
+ * MHD_E_STATE (after filling ms/launches with what was recorded).  mhd_profile_read
+ * synchronises, adds up the intervals recorded since enable, and returns total milliseconds
+ * and recorded units per class.  Enabling resets the totals.  MHD_E_ARG for enable < 0. */
 int mhd_profile_enable(mhd_ctx* ctx, int32_t enable);
 int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
 

@@ -74,6 +74,8 @@ def lib():
         L.orc_face_flux.restype = C.c_int
         L.orc_face_flux_batch.argtypes = [C.POINTER(Config), _D, _D, C.c_int64, C.c_double, _D]
         L.orc_face_flux_batch.restype = C.c_int64
+        L.orc_hlld_fan.argtypes = [C.POINTER(Config), _D, _D, C.c_double, _D]
+        L.orc_hlld_fan.restype = None
         L.orc_compute_dt.argtypes = [C.POINTER(Config), _D, _D, _D, C.POINTER(Counters)]
         L.orc_compute_dt.restype = C.c_int
         L.orc_step.argtypes = [C.POINTER(Config), _D, C.c_double, C.c_double, C.POINTER(Counters)]
@@ -209,6 +211,24 @@ def face_flux(problem, VL, VR, ch):
     F = np.zeros_like(VL)
     nfb = lib().orc_face_flux_batch(C.byref(cfg), _ptr(VL), _ptr(VR), VL.shape[0], ch, _ptr(F))
     return F, int(nfb)
+
+
+def hlld_fan(problem, VL, VR, ch):
+    """Test-only: the HLLD wave fan of one face pair (normal frame).  Returns a dict with the
+    speeds SL, SsL, SM, SsR, SR, pts, the branch `flag` (0 fan, 1 SM guard, 2 wave-ordering
+    guard, 3 supersonic), the R6 flags degL / degR and the states UL, UsL, UssL, UssR, UsR, UR
+    and fluxes FL, FR (8 components each)."""
+    cfg = make_config(problem)
+    VL = np.ascontiguousarray(VL, dtype=np.float64)
+    VR = np.ascontiguousarray(VR, dtype=np.float64)
+    out = np.zeros(73, dtype=np.float64)
+    lib().orc_hlld_fan(C.byref(cfg), _ptr(VL), _ptr(VR), ch, _ptr(out))
+    d = dict(zip(("SL", "SsL", "SM", "SsR", "SR", "pts"), out[:6]))
+    d["flag"], d["degL"], d["degR"] = int(out[6]), bool(out[7]), bool(out[8])
+    A = out[9:].reshape(8, 8)
+    for j, k in enumerate(("UL", "UsL", "UssL", "UssR", "UsR", "UR", "FL", "FR")):
+        d[k] = A[j].copy()
+    return d
 
 
 def compute_dt(problem, U):

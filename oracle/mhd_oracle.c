@@ -417,6 +417,90 @@ int orc_face_flux(const orc_config* c, const double* VLin, const double* VRin, d
   return fell_back;
 }
 
+/* Test-only: the HLLD wave fan of one face pair (the same side_state / star_state as
+ * orc_face_flux, the double-star states by the same expressions), so that tests can pin the
+ * states themselves (integral consistency, jump conditions, the R6 / R7 branches):
+ * out[0..4] = SL, S*L, SM, S*R, SR; out[5] = p_t*; out[6] = 0 fan built, 1 SM outside (SL, SR),
+ * 2 wave-ordering guard, 3 supersonic (SL > 0 or SR < 0, no fan); out[7], out[8] = R6 degenerate
+ * flag of the left / right star state; out[9 + 8 j + k] for j = 0..7: UL, U*L, U**L, U**R, U*R,
+ * UR, FL, FR (the 8 MHD components, normal frame, B_n = Bm).  Entries not reached stay 0. */
+void orc_hlld_fan(const orc_config* c, const double* VLin, const double* VRin, double ch, double* out) {
+  memset(out, 0, 73 * sizeof(double));
+  const double gamma = c->gamma;
+  const double igm1 = 1.0 / (gamma - 1.0);
+  double Bm;
+  if (c->glm) {
+    const double ihc = 0.5 / ch;
+    Bm = 0.5 * (VLin[5] + VRin[5]) - ihc * (VRin[8] - VLin[8]);
+  } else {
+    Bm = 0.5 * (VLin[5] + VRin[5]);
+  }
+  side_t L, R;
+  side_state(gamma, igm1, VLin, Bm, &L);
+  side_state(gamma, igm1, VRin, Bm, &R);
+  double* A = out + 9;
+  for (int k = 0; k < 8; ++k) {
+    A[0 * 8 + k] = L.U[k];
+    A[5 * 8 + k] = R.U[k];
+    A[6 * 8 + k] = L.F[k];
+    A[7 * 8 + k] = R.F[k];
+  }
+  const double cmax = fmax(L.cf, R.cf);
+  const double SL = fmin(L.vn, R.vn) - cmax;
+  const double SR = fmax(L.vn, R.vn) + cmax;
+  out[0] = SL;
+  out[4] = SR;
+  if (SL > 0.0 || SR < 0.0) {
+    out[6] = 3.0;
+    return;
+  }
+  const double B = Bm;
+  const double sdL = SL - L.vn, sdR = SR - R.vn;
+  const double mL = L.rho * sdL, mR = R.rho * sdR;
+  const double iden = 1.0 / (mR - mL);
+  const double SM = (((mR * R.vn - mL * L.vn) - R.pt) + L.pt) * iden;
+  const double pts = ((mR * L.pt - mL * R.pt) + (mL * mR) * (R.vn - L.vn)) * iden;
+  out[2] = SM;
+  out[5] = pts;
+  if (!(SL < SM && SM < SR)) {
+    out[6] = 1.0;
+    return;
+  }
+  star_t sL, sR;
+  star_state(&L, SL, SM, pts, B, &sL);
+  star_state(&R, SR, SM, pts, B, &sR);
+  out[7] = fabs(sL.m * sL.sm - B * B) < 1e-8 * pts ? 1.0 : 0.0;
+  out[8] = fabs(sR.m * sR.sm - B * B) < 1e-8 * pts ? 1.0 : 0.0;
+  const double srL = sqrt(sL.rhos), srR = sqrt(sR.rhos);
+  const double SsL = SM - fabs(B) / srL;
+  const double SsR = SM + fabs(B) / srR;
+  out[1] = SsL;
+  out[3] = SsR;
+  for (int k = 0; k < 8; ++k) {
+    A[1 * 8 + k] = sL.Us[k];
+    A[4 * 8 + k] = sR.Us[k];
+  }
+  if (!(SL <= SsL && SsR <= SR)) {
+    out[6] = 2.0;
+    return;
+  }
+  const double sg = (B >= 0.0) ? 1.0 : -1.0;
+  const double is = 1.0 / (srL + srR);
+  const double vss1 = ((srL * sL.vst1 + srR * sR.vst1) + (sR.bst1 - sL.bst1) * sg) * is;
+  const double vss2 = ((srL * sL.vst2 + srR * sR.vst2) + (sR.bst2 - sL.bst2) * sg) * is;
+  const double bss1 = ((srL * sR.bst1 + srR * sL.bst1) + ((srL * srR) * (sR.vst1 - sL.vst1)) * sg) * is;
+  const double bss2 = ((srL * sR.bst2 + srR * sL.bst2) + ((srL * srR) * (sR.vst2 - sL.vst2)) * sg) * is;
+  const double vBss = (SM * B + vss1 * bss1) + vss2 * bss2;
+  const double EssL = sL.Es - (srL * (sL.vBs - vBss)) * sg;
+  const double EssR = sR.Es + (srR * (sR.vBs - vBss)) * sg;
+  const double UssL[8] = {sL.rhos, sL.rhos * SM, sL.rhos * vss1, sL.rhos * vss2, EssL, B, bss1, bss2};
+  const double UssR[8] = {sR.rhos, sR.rhos * SM, sR.rhos * vss1, sR.rhos * vss2, EssR, B, bss1, bss2};
+  for (int k = 0; k < 8; ++k) {
+    A[2 * 8 + k] = UssL[k];
+    A[3 * 8 + k] = UssR[k];
+  }
+}
+
 int64_t orc_face_flux_batch(const orc_config* c, const double* VL, const double* VR, int64_t n, double ch,
                             double* F) {
   const int nvar = 8 + (c->glm ? 1 : 0);

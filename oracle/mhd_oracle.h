@@ -72,6 +72,9 @@ double orc_limited_slope(int32_t limiter, double dm, double dp);
  * F receives nvar components in the normal frame.  Returns 1 if HLLD fell back to HLL. */
 int orc_face_flux(const orc_config* c, const double* VL, const double* VR, double ch, double* F);
 /* batched variant: VL/VR/F are [n][nvar] rows. returns number of HLL fallbacks. */
+/* test-only: the HLLD wave fan of one face pair (speeds, branch flags, the six states and
+ * the two side fluxes; layout in mhd_oracle.c) — 73 doubles */
+void orc_hlld_fan(const orc_config* c, const double* VL, const double* VR, double ch, double* out);
 int64_t orc_face_flux_batch(const orc_config* c, const double* VL, const double* VR, int64_t n,
                             double ch, double* F);
 /* c.13: M = max_cells sum_d s_d/dx_d and ch = max_cells max_d s_d; dt = cfl/M. */

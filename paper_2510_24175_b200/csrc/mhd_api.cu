@@ -89,6 +89,7 @@ struct mhd_ctx {
   std::vector<int> ev_kind;  // one entry per recorded (start, stop) pair
   double prof_ms[2] = {0, 0};
   int64_t prof_n[2] = {0, 0};
+  int64_t prof_dropped = 0;
 };
 
 namespace {
@@ -277,8 +278,11 @@ int exchange_nccl(mhd_ctx* c, double* U) {
   return MHD_OK;
 }
 
-// exchange part for an in-process group: receives are device copies from the peer slab's
-// array (the same array role: U^n or U*)
+// exchange part for an in-process group (MHD_TRANSPORT_LOCAL): the same plan and the same
+// stream/event protocol as exchange_nccl (comm stream after `ev_ready`, `ev_halo` recorded
+// after the last transfer), with each receive a device copy from the peer slab's array of the
+// same role.  The group shares one compute stream, so `ev_ready` of a slab follows every launch
+// of the previous stage of every slab.
 int exchange_local(mhd_ctx* c, int stage) {
   const size_t pe = plane_elems(c), pb = pe * sizeof(double);
   const int g = c->gz;
@@ -286,6 +290,8 @@ int exchange_local(mhd_ctx* c, int stage) {
   if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, g, plan))
     return set_err(c, MHD_E_ARG, "halo plan");
   double* mine = stage_plan(c, stage).in;
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_ready, c->stream));
+  CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
   for (int i = 0; i < 4; ++i) {
     if (plan[i][0] < 0 || plan[i][1] != 1) continue;  // receives only
     const mhd_ctx* peer = c->group[plan[i][0]];
@@ -295,20 +301,28 @@ int exchange_local(mhd_ctx* c, int stage) {
     // ghosts (recv from up) <- up's storage planes g..2g-1
     const int src = (plan[i][2] == 0) ? peer->nzl : g;
     CUDA_OR_RETURN(c, cudaMemcpyAsync(mine + (size_t)plan[i][2] * pe, theirs + (size_t)src * pe, g * pb,
-                                      cudaMemcpyDeviceToDevice, c->stream));
+                                      cudaMemcpyDeviceToDevice, c->comm_stream));
   }
+  CUDA_OR_RETURN(c, cudaEventRecord(c->ev_halo, c->comm_stream));
   return MHD_OK;
 }
 
-// kernel timing: record a start event before a launch of class `kind`, the stop after it
+// the halo of stage `stage`'s input array (stage 1: U^n) on the comm stream, by the context's
+// transport; `ev_halo` marks its completion
+int exchange(mhd_ctx* c, int stage) {
+  return c->transport == MHD_TRANSPORT_LOCAL ? exchange_local(c, stage) : exchange_nccl(c, stage_plan(c, stage).in);
+}
+
+// kernel timing: one (start, stop) event pair per timed unit — a whole RK stage (all its
+// launches, including the wait for its halo) or a dt pass.  The pool is created by
+// mhd_profile_enable; a unit beyond its capacity is not recorded (no event is created and
+// nothing synchronises while a timed loop runs).
 int prof_begin(mhd_ctx* c, int kind) {
   if (!c->prof) return -1;
   const size_t pair = c->ev_kind.size();
-  if (pair >= 4096) return -1;  // cap; read() drains
-  while (c->ev_pool.size() < 2 * (pair + 1)) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return -1;
-    c->ev_pool.push_back(e);
+  if (2 * (pair + 1) > c->ev_pool.size()) {
+    c->prof_dropped += 1;
+    return -1;
   }
   cudaEventRecord(c->ev_pool[2 * pair], c->stream);
   c->ev_kind.push_back(kind);
@@ -328,13 +342,14 @@ void prof_drain(mhd_ctx* c) {
   c->ev_kind.clear();
 }
 
-// CT: the z ghost planes of U complete before the launch (periodic copy on one GPU; the NCCL
-// halo on slabs, waited for on the compute stream: the CT stage has no interior/boundary split)
-int ct_fill_ghosts(mhd_ctx* c, double* U) {
-  int rc = fill_z_ghosts_local(c, U);
+// CT and split WENO-Z: the z ghost planes of stage `stage`'s input complete before the launches
+// (periodic copy on one slab; the halo on slabs, waited for on the compute stream: these stages
+// have no interior/boundary split)
+int whole_fill_ghosts(mhd_ctx* c, int stage) {
+  int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
-  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
-    if ((rc = exchange_nccl(c, U))) return rc;
+  if (c->nranks > 1) {
+    if ((rc = exchange(c, stage))) return rc;
     CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
   }
   return MHD_OK;
@@ -367,12 +382,36 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
-  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
-  const int pr = prof_begin(c, 0);
   cudaError_t e = mhd::launch_stage(c->dim, c->nv, c->scheme.riemann, a, c->stream);
-  prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "stage %d launch: %s", stage, cudaGetErrorString(e));
   return MHD_OK;
+}
+
+// One RK stage of the fused kernel on a slab, the schedule every multi-slab run uses (NCCL
+// ranks and the in-process group alike, the boundary exchange overlapped with
+// the interior): the local z ghost copies, then the halo on the comm stream while the interior
+// planes [g, nz-g) run (their stencil reads no ghost plane), then — after `ev_halo` — the g + g
+// boundary planes.  One slab: the ghost copies and one whole launch.  One profiling pair spans
+// the stage.
+int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+  int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
+  if (rc) return rc;
+  if (c->nranks > 1 && c->dim == 3) {
+    if ((rc = exchange(c, stage))) return rc;
+    const int pr = prof_begin(c, 0);
+    const int g = c->gz;
+    const int lo = g < c->nzl ? g : c->nzl, hi = c->nzl - g > lo ? c->nzl - g : lo;
+    if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
+    CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
+    if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
+    prof_end(c, pr);
+    return MHD_OK;
+  }
+  const int pr = prof_begin(c, 0);
+  rc = run_stage(c, stage, k, 0, c->nzl);
+  prof_end(c, pr);
+  return rc;
 }
 
 // the two auxiliary streams (and fork/join events) on which the split and CT stages run their
@@ -443,7 +482,6 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
-  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
   const int pr = prof_begin(c, 0);
   if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
@@ -468,7 +506,6 @@ int reduce_and_read(mhd_ctx* c) {
   for (int i = 0; i < 3; ++i) d.idx[i] = 1.0 / c->dx[i];
   d.out = c->dbuf;
   d.bad = c->dbuf + 5;
-  if (c->prof && c->ev_kind.size() >= 4000) prof_drain(c);
   const int pr = prof_begin(c, 1);
   cudaError_t e = c->scheme.ct ? mhd::launch_ct_dt(d, c->nsm, c->stream) : mhd::launch_dt(c->dim, c->nv, d, c->nsm, c->stream);
   prof_end(c, pr);
@@ -733,13 +770,15 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     return MHD_E_CUDA;
   }
   c->transport = dist ? dist->transport : MHD_TRANSPORT_NCCL;
-  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
+  if (c->nranks > 1) {  // the halo's stream and events (NCCL ranks and in-process slabs alike)
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
       mhd_destroy(c);
       return MHD_E_CUDA;
     }
+  }
+  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
     ncclUniqueId id;
     memcpy(&id, dist->nccl_id, sizeof id);
     if (ncclCommInitRank(&c->comm, c->nranks, id, c->rank) != ncclSuccess) {
@@ -962,7 +1001,7 @@ int mhd_compute_dt(mhd_ctx* c, double* dt) {
   rc = check_sticky(c);
   if (rc) return rc;
   if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
-  if (c->scheme.ct && (rc = ct_fill_ghosts(c, c->U0))) return rc;  // cell-centred B_z needs plane nz
+  if (c->scheme.ct && (rc = whole_fill_ghosts(c, 1))) return rc;  // cell-centred B_z needs plane nz
   rc = reduce_and_read(c);
   if (rc) return rc;
   double M, S;
@@ -995,30 +1034,12 @@ int mhd_step(mhd_ctx* c, double dt) {
   }
   if (c->scheme.glm && !(c->ch > 0.0)) return set_err(c, MHD_E_ARG, "c_h must be positive");
   const StageConsts k = make_consts(c, dt, c->ch);
-  if (c->scheme.ct || c->split) {
-    for (int stage = 1; stage <= nstages(c); ++stage) {
-      if ((rc = ct_fill_ghosts(c, stage_plan(c, stage).in))) return rc;
-      if ((rc = c->split ? run_split_stage(c, stage, k) : run_ct_stage(c, stage, k))) return rc;
-    }
-    c->ch_valid = false;
-    c->diag.steps += 1;
-    return MHD_OK;
-  }
   for (int stage = 1; stage <= nstages(c); ++stage) {
-    double* U = stage_plan(c, stage).in;
-    if ((rc = fill_z_ghosts_local(c, U))) return rc;
-    if (c->nranks > 1 && c->dim == 3) {
-      // halo exchange on the comm stream, overlapped with the interior planes [g, nz-g)
-      // (their stencil never reads a ghost plane); then the g + g boundary planes
-      if ((rc = exchange_nccl(c, U))) return rc;
-      const int g = c->gz;
-      const int lo = g < c->nzl ? g : c->nzl, hi = c->nzl - g > lo ? c->nzl - g : lo;
-      if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
-      CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
-      if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
-      if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
-    } else {
-      if ((rc = run_stage(c, stage, k, 0, c->nzl))) return rc;
+    if (c->scheme.ct || c->split) {
+      if ((rc = whole_fill_ghosts(c, stage))) return rc;
+      if ((rc = c->split ? run_split_stage(c, stage, k) : run_ct_stage(c, stage, k))) return rc;
+    } else if ((rc = fused_stage(c, stage, k))) {
+      return rc;
     }
   }
   c->ch_valid = false;
@@ -1077,10 +1098,8 @@ int mhd_group_compute_dt(mhd_ctx* const* ctxs, int32_t n, double* dt) {
   if (rc || !dt) return rc ? rc : MHD_E_ARG;
   double M = 0.0, S = 0.0;
   if (ctxs[0]->scheme.ct) {  // CT: U^n ghost planes (cell-centred B_z of the last plane)
-    for (int r = 0; r < n; ++r) {
-      if ((rc = fill_z_ghosts_local(ctxs[r], ctxs[r]->U0))) return rc;
-      if (n > 1 && (rc = exchange_local(ctxs[r], 1))) return rc;
-    }
+    for (int r = 0; r < n; ++r)
+      if ((rc = whole_fill_ghosts(ctxs[r], 1))) return rc;
   }
   for (int r = 0; r < n; ++r) {  // exact maxima: the order over slabs does not matter
     mhd_ctx* c = ctxs[r];
@@ -1106,18 +1125,18 @@ int mhd_group_step(mhd_ctx* const* ctxs, int32_t n, double dt) {
   if (!(dt > 0.0) || !std::isfinite(dt)) return MHD_E_ARG;
   for (int r = 0; r < n; ++r)
     if (!ctxs[r]->ch_valid) return set_err(ctxs[r], MHD_E_STATE, "call mhd_group_compute_dt first");
+  // per stage, slab by slab, exactly the schedule of an NCCL rank's mhd_step (fused_stage /
+  // whole_fill_ghosts with the device-copy halo on each slab's comm stream)
   for (int stage = 1; stage <= nstages(ctxs[0]); ++stage) {
     for (int r = 0; r < n; ++r) {
       mhd_ctx* c = ctxs[r];
-      if ((rc = fill_z_ghosts_local(c, stage_plan(c, stage).in))) return rc;
-      if (n > 1 && (rc = exchange_local(c, stage))) return rc;
-    }
-    for (int r = 0; r < n; ++r) {
-      mhd_ctx* c = ctxs[r];
       const StageConsts k = make_consts(c, dt, c->ch);
-      if ((rc = c->scheme.ct ? run_ct_stage(c, stage, k)
-                             : (c->split ? run_split_stage(c, stage, k) : run_stage(c, stage, k, 0, c->nzl))))
+      if (c->scheme.ct || c->split) {
+        if ((rc = whole_fill_ghosts(c, stage))) return rc;
+        if ((rc = c->split ? run_split_stage(c, stage, k) : run_ct_stage(c, stage, k))) return rc;
+      } else if ((rc = fused_stage(c, stage, k))) {
         return rc;
+      }
     }
   }
   for (int r = 0; r < n; ++r) {
@@ -1189,16 +1208,20 @@ void mhd_destroy(mhd_ctx* c) {
 }
 
 int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
-  if (!c) return MHD_E_ARG;
+  if (!c || enable < 0) return MHD_E_ARG;
   if (c->prof) prof_drain(c);
   c->prof = enable != 0;
-  while (c->prof && c->ev_pool.size() < 256) {  // created up front: none inside a timed loop
+  // the whole pool up front: none is created (and nothing drains) inside a timed loop
+  const size_t pairs = enable > 1 ? (size_t)enable : 1024;
+  while (c->prof && c->ev_pool.size() < 2 * pairs) {
     cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) break;
+    if (cudaEventCreate(&e) != cudaSuccess) return set_err(c, MHD_E_CUDA, "profile: event pool");
     c->ev_pool.push_back(e);
   }
+  c->ev_kind.clear();
   c->prof_ms[0] = c->prof_ms[1] = 0.0;
   c->prof_n[0] = c->prof_n[1] = 0;
+  c->prof_dropped = 0;
   return MHD_OK;
 }
 
@@ -1209,6 +1232,9 @@ int mhd_profile_read(mhd_ctx* c, double ms[2], int64_t launches[2]) {
     ms[i] = c->prof_ms[i];
     launches[i] = c->prof_n[i];
   }
+  if (c->prof_dropped)
+    return set_err(c, MHD_E_STATE, "profile: %lld timed units exceeded the event pool (mhd_profile_enable capacity)",
+                   (long long)c->prof_dropped);
   return MHD_OK;
 }
 

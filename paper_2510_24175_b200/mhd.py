@@ -295,11 +295,13 @@ class Solver:
                                                 VL.shape[0], float(ch), C.c_void_p(F.data_ptr()), C.byref(nh)))
         return F, nh.value
 
-    def profile_enable(self, on: bool = True) -> None:
-        self._check(self._L.mhd_profile_enable(self._h, 1 if on else 0))
+    def profile_enable(self, on: bool = True, capacity: int = 0) -> None:
+        """capacity: timed units (RK stages + dt passes) to make room for (0: the default 1024)."""
+        self._check(self._L.mhd_profile_enable(self._h, (capacity if capacity > 1 else 1) if on else 0))
 
     def profile_read(self):
-        """{'stage': (ms, launches), 'dt': (ms, launches)} since profile_enable."""
+        """{'stage': (ms, stages), 'dt': (ms, passes)} since profile_enable (one event pair per RK
+        stage, whatever its launch count, and per dt pass)."""
         ms, n = (C.c_double * 2)(), (C.c_int64 * 2)()
         self._check(self._L.mhd_profile_read(self._h, ms, n))
         return {"stage": (ms[0], n[0]), "dt": (ms[1], n[1])}

@@ -695,8 +695,11 @@ def test_ot3d_1024_full_size_sampled(mhd):
 # ---------------------------------------------------------------------------------------------
 # decomposition invariance: P z-slabs == 1 domain, bitwise
 # ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_slab_group_bitwise_equals_single_domain(mhd, P):
+    """The group runs every slab through the NCCL ranks' stage schedule (mhd_api.cu fused_stage):
+    interior planes [2, nz-2) while the halo copies run on the slab's comm stream, then the two
+    2-plane boundary launches after the halo event.  P = 8: 4-plane slabs, an empty interior."""
     p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
     U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
     s = mhd.Solver(p)
@@ -917,3 +920,78 @@ def test_ct_slab_group_bitwise(mhd, case, P):
     assert np.array_equal(log1, logP) and np.array_equal(U1, UP)
     for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
         assert d1[k] == dP[k], (k, d1[k], dP[k])
+
+
+def test_slab_group_interior_split_with_z_chunks(mhd):
+    """The interior/boundary split of the slab schedule combined with small z chunks (MHD_KZ=3:
+    the interior range [2, 10) starts a chunk at z = 2 and the boundary launches are chunks of
+    their own), on slabs of 12 planes: bitwise equal to one domain with equal counters."""
+    p, U0 = _harsh_state(I.MC, 1, -13, 3.0, -2)
+    p = p.replace(n=(p.n[0], p.n[1], 36))
+    U0 = np.ascontiguousarray(np.concatenate([U0] * (36 // U0.shape[1] + 1), axis=1)[:, :36])
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(3)
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    os.environ["MHD_KZ"] = "3"
+    try:
+        g = mhd.SolverGroup(p, 3)
+    finally:
+        os.environ.pop("MHD_KZ", None)
+    g.set_state(U0)
+    logP = g.run(3)
+    UP, dP = g.get_state(), g.diag()
+    g.destroy()
+    assert np.array_equal(log1, logP) and np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k], (k, d1[k], dP[k])
+
+
+@pytest.mark.parametrize("scheme", ["plm-rk2", "wenoz-rk3", "ct-rk2"])
+def test_profile_units(mhd, scheme):
+    """mhd_profile_*: one event pair per RK stage (whatever its launch count) and per dt pass;
+    a run beyond the pool's capacity is reported, not silently truncated."""
+    p = I.orszag_tang_3d(16)
+    if scheme == "wenoz-rk3":
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    if scheme == "ct-rk2":
+        p = I.ct_problem(p)
+    U0 = I.orszag_tang_3d_ic(p.replace(ct=0, glm=1) if p.ct else p)
+    U0 = np.ascontiguousarray(U0[:8] if p.ct else U0)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    s.run(1)
+    s.profile_enable(True, capacity=64)
+    s.run(5)
+    prof = s.profile_read()
+    ns = 3 if p.stepper == I.RK3 else 2
+    assert prof["stage"][1] == 5 * ns and prof["dt"][1] == 5, prof
+    assert prof["stage"][0] > 0 and prof["dt"][0] > 0
+    s.profile_enable(True, capacity=4)
+    s.run(2)
+    with pytest.raises(mhd.MhdError):
+        s.profile_read()
+    s.profile_enable(False)
+    s.destroy()
+
+
+def test_nccl_two_ranks_bitwise(mhd, tmp_path):
+    """Two NCCL ranks (torchrun, one GPU each) run the real multi-rank path — NCCL send/recv halo
+    on the comm stream overlapped with the interior launch, ncclAllReduce for dt and counters —
+    and must equal one domain bitwise (tools/nccl_parity.py).  Needs two GPUs (gpurun and the
+    driver's GPU tier provide one: skipped there; NCCL refuses two ranks on one device)."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "nccl_parity.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tools", "nccl_parity.py"),
+           "--out", str(out)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=root)
+    import json
+    res = json.loads(out.read_text())
+    assert all(r["bitwise"] for r in res["cases"]), res
