@@ -86,10 +86,11 @@ struct mhd_ctx {
   // kernel timing (mhd_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
-  std::vector<int> ev_kind;  // one entry per recorded (start, stop) pair
-  double prof_ms[2] = {0, 0};
-  int64_t prof_n[2] = {0, 0};
+  std::vector<int> ev_kind;  // one entry per recorded (start, stop) pair: its class
+  double prof_ms[4] = {0, 0, 0, 0};  // per timed class: 0 dt pass, 1..3 RK stage
+  int64_t prof_n[4] = {0, 0, 0, 0};
   int64_t prof_dropped = 0;
+  size_t prof_cap = 0;  // pairs the pool has room for (mhd_profile_enable)
 };
 
 namespace {
@@ -320,7 +321,7 @@ int exchange(mhd_ctx* c, int stage) {
 int prof_begin(mhd_ctx* c, int kind) {
   if (!c->prof) return -1;
   const size_t pair = c->ev_kind.size();
-  if (2 * (pair + 1) > c->ev_pool.size()) {
+  if (pair >= c->prof_cap) {
     c->prof_dropped += 1;
     return -1;
   }
@@ -398,7 +399,7 @@ int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   if (rc) return rc;
   if (c->nranks > 1 && c->dim == 3) {
     if ((rc = exchange(c, stage))) return rc;
-    const int pr = prof_begin(c, 0);
+    const int pr = prof_begin(c, stage);
     const int g = c->gz;
     const int lo = g < c->nzl ? g : c->nzl, hi = c->nzl - g > lo ? c->nzl - g : lo;
     if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
@@ -408,7 +409,7 @@ int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
     prof_end(c, pr);
     return MHD_OK;
   }
-  const int pr = prof_begin(c, 0);
+  const int pr = prof_begin(c, stage);
   rc = run_stage(c, stage, k, 0, c->nzl);
   prof_end(c, pr);
   return rc;
@@ -446,7 +447,7 @@ int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
-  const int pr = prof_begin(c, 0);
+  const int pr = prof_begin(c, stage);
   if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_ct_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
   prof_end(c, pr);
@@ -482,7 +483,7 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
-  const int pr = prof_begin(c, 0);
+  const int pr = prof_begin(c, stage);
   if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
   prof_end(c, pr);
@@ -506,7 +507,7 @@ int reduce_and_read(mhd_ctx* c) {
   for (int i = 0; i < 3; ++i) d.idx[i] = 1.0 / c->dx[i];
   d.out = c->dbuf;
   d.bad = c->dbuf + 5;
-  const int pr = prof_begin(c, 1);
+  const int pr = prof_begin(c, 0);
   cudaError_t e = c->scheme.ct ? mhd::launch_ct_dt(d, c->nsm, c->stream) : mhd::launch_dt(c->dim, c->nv, d, c->nsm, c->stream);
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt launch: %s", cudaGetErrorString(e));
@@ -1218,24 +1219,39 @@ int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
     if (cudaEventCreate(&e) != cudaSuccess) return set_err(c, MHD_E_CUDA, "profile: event pool");
     c->ev_pool.push_back(e);
   }
+  c->prof_cap = pairs;
   c->ev_kind.clear();
-  c->prof_ms[0] = c->prof_ms[1] = 0.0;
-  c->prof_n[0] = c->prof_n[1] = 0;
+  for (int i = 0; i < 4; ++i) {
+    c->prof_ms[i] = 0.0;
+    c->prof_n[i] = 0;
+  }
   c->prof_dropped = 0;
   return MHD_OK;
 }
 
-int mhd_profile_read(mhd_ctx* c, double ms[2], int64_t launches[2]) {
-  if (!c || !ms || !launches) return MHD_E_ARG;
+int mhd_profile_read_stages(mhd_ctx* c, double ms[4], int64_t units[4]) {
+  if (!c || !ms || !units) return MHD_E_ARG;
   prof_drain(c);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 4; ++i) {
     ms[i] = c->prof_ms[i];
-    launches[i] = c->prof_n[i];
+    units[i] = c->prof_n[i];
   }
   if (c->prof_dropped)
     return set_err(c, MHD_E_STATE, "profile: %lld timed units exceeded the event pool (mhd_profile_enable capacity)",
                    (long long)c->prof_dropped);
   return MHD_OK;
+}
+
+int mhd_profile_read(mhd_ctx* c, double ms[2], int64_t launches[2]) {
+  if (!c || !ms || !launches) return MHD_E_ARG;
+  double m4[4];
+  int64_t n4[4];
+  const int rc = mhd_profile_read_stages(c, m4, n4);
+  ms[0] = m4[1] + m4[2] + m4[3];
+  launches[0] = n4[1] + n4[2] + n4[3];
+  ms[1] = m4[0];
+  launches[1] = n4[0];
+  return rc;
 }
 
 int mhd_debug_face_flux(mhd_ctx* c, const double* VL, const double* VR, int64_t n, double ch, double* F,

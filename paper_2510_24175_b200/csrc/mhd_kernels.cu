@@ -251,6 +251,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   const size_t pstride = (size_t)fs * NV;
   const int kb = a.zb + blockIdx.z * a.kz;  // this CTA's z chunk inside [zb, ze)
   const int ke = min(kb + a.kz, a.ze);
+#ifdef MHD_STAGGER_NS
+  // measurement only: the second half of the grid starts later (de-phases co-resident CTAs)
+  if ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x >= gridDim.x * gridDim.y * gridDim.z / 2)
+    __nanosleep(MHD_STAGGER_NS);
+#endif
   // rare events (floors, fallbacks, HLL fallbacks, bad cells) go to shared-memory counters by
   // atomics only when they happen: no registers held for them across the face solves
   __shared__ int s_cnt[3];

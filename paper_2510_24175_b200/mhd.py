@@ -30,7 +30,7 @@ EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
            "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
            "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join",
-           "mhd_workspace_bytes", "mhd_bind_workspace", "mhd_run")
+           "mhd_workspace_bytes", "mhd_bind_workspace", "mhd_run", "mhd_profile_read_stages")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -111,6 +111,7 @@ def load() -> C.CDLL:
         L.mhd_debug_fast_ops.argtypes = [P, P, C.c_int64, P, P]
     L.mhd_profile_enable.argtypes = [P, C.c_int32]
     L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.mhd_profile_read_stages.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.mhd_group_compute_dt.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(C.c_double)]
     L.mhd_group_step.argtypes = [C.POINTER(P), C.c_int32, C.c_double]
     L.mhd_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
@@ -305,6 +306,12 @@ class Solver:
         ms, n = (C.c_double * 2)(), (C.c_int64 * 2)()
         self._check(self._L.mhd_profile_read(self._h, ms, n))
         return {"stage": (ms[0], n[0]), "dt": (ms[1], n[1])}
+
+    def profile_read_stages(self):
+        """{'dt': (ms, passes), 'stage1': (ms, stages), 'stage2': ..., 'stage3': ...} since profile_enable."""
+        ms, n = (C.c_double * 4)(), (C.c_int64 * 4)()
+        self._check(self._L.mhd_profile_read_stages(self._h, ms, n))
+        return {"dt": (ms[0], n[0]), "stage1": (ms[1], n[1]), "stage2": (ms[2], n[2]), "stage3": (ms[3], n[3])}
 
     def destroy(self) -> None:
         if getattr(self, "_h", None):
