@@ -25,8 +25,10 @@
 // All arithmetic is the recipe of DESIGN.md §3 (see mhd_device.cuh), built with
 // --fmad=false so that results equal the CPU oracle bitwise.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
@@ -179,6 +181,37 @@ __device__ __noinline__ FaceOut<NV> exact_face(StageConsts c, const double* Vc, 
 }
 
 // ---------------------------------------------------------------------------------------
+// TMA (sm_90+ bulk tensor copies) and mbarrier helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
+}
+// one plane window [f][PH][PW] of the tensor at (x, y, 0, plane) into smem; completes on mb
+__device__ __forceinline__ void tma_load_window(void* dst, const CUtensorMap* map, int x, int y, int plane,
+                                                uint64_t* mb, uint32_t bytes) {
+  // the CTA's generic-proxy accesses of dst (ordered before this thread by a barrier) happen
+  // before the async-proxy writes of the copy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(0), "r"(plane), "r"(smem_u32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(mb)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// ---------------------------------------------------------------------------------------
 // fused stage kernel
 #ifndef MHD_JOB_UNROLL
 #define MHD_JOB_UNROLL 1
@@ -223,8 +256,8 @@ struct StageOcc {
 // so every warp runs at most 3 face solves per plane and the per-plane barriers do not wait
 // on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
-template <int DIM, int NV, int RS, int TY, int REC>
-__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)) k_stage(StageArgs a) {
+template <int DIM, int NV, int RS, int TY, int REC, bool TMA>
+__global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)) k_stage(const __grid_constant__ StageArgs a) {
   // REC: reconstruction, a compile-time choice (0 PLM minmod, 1 PLM MC, 2 WENO-Z)
   constexpr bool WZ = REC == 2;
   constexpr int LIM = REC == 0 ? 0 : 1;
@@ -232,8 +265,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   using S = StageSmem<DIM, NV, TY, G>;
   constexpr int TX = S::TX, HY = S::HY, PW = S::PW, PH = S::PH, NT = S::NT;
   constexpr int NC = 32 * TY;        // threads of the cell warps
-  extern __shared__ double smem[];
-  double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo)
+  extern __shared__ __align__(128) double smem[];
+  double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo); TMA destination
   double* Vpz = Vc + S::nVc;         // [NV][NC] V+ (z normal frame) of plane k   (3D)
   double* Fz = Vpz + S::nCol;        // [2][NV][NC] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
   double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
@@ -260,9 +293,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // atomics only when they happen: no registers held for them across the face solves
   __shared__ int s_cnt[3];
   __shared__ unsigned long long s_bad;
+  __shared__ uint64_t s_mbar;  // TMA plane-window completion
+  constexpr bool tma = DIM == 3 && TMA;  // the plane window by TMA (a.tmap) instead of per-thread loads
+  uint32_t tma_parity = 0;
   if (tid == 0) {
     s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
     s_bad = ULLONG_MAX;
+    if (tma) mbar_init(&s_mbar, 1);
   }
   __syncthreads();
 
@@ -310,6 +347,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     }
     constexpr int NXH = 2 * G * TY;
     constexpr int NYH = (DIM >= 2) ? 2 * G * TX : 0;
+#ifdef MHD_WI_NOHALO  // what-if (timing only): the halo keeps the previous plane
+    if (false)
+#endif
     for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {  // the edge warp takes the first slots
       double v[NV];
       if (h < NXH) {
@@ -322,6 +362,45 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         const int r = (rs < G) ? rs : TY + rs;  // padded rows 0..G-1 | TY+G..TY+2G-1
         convert_any(k, x0 + col, y0 + r - HY, v);
         store_vc(r, col + G, v);
+      }
+    }
+  };
+  // The same plane window through TMA (3D): one elected thread copies the raw conservative
+  // window [f][PH][PW] of plane k (halo and unused corners included; out-of-domain elements
+  // zero-filled) into Vc, after the barrier that ends every read of Vc; each slot the face jobs
+  // read is then converted in place from shared memory, or — out of the domain (periodic wrap,
+  // outflow clamp, ragged tails) — from global memory as in load_plane.  tma_issue and
+  // tma_convert bracket work that does not touch Vc (the update), which hides the copy.
+  constexpr uint32_t kWinBytes = (uint32_t)(sizeof(double) * NV * PH * PW);
+  auto tma_issue = [&](int k) {
+    if (tid == 0) tma_load_window(Vc, &a.tmap, x0 - G, y0 - HY, a.gz + k, &s_mbar, kWinBytes);
+  };
+  auto convert_slot = [&](int k, int r, int col) {  // Vc slot (r, col): global (x0 + col - G, y0 + r - HY)
+    const int x = x0 + col - G, y = y0 + r - HY;
+    double v[NV];
+    if (x >= 0 && x < nx && y >= 0 && y < ny) {
+      double u[NV];
+#pragma unroll
+      for (int f = 0; f < NV; ++f) u[f] = Vc[(f * PH + r) * PW + col];
+      cons2prim<NV>(u, v, c.gm1, c.p_floor);
+    } else {
+      convert_any(k, x, y, v);
+    }
+    store_vc(r, col, v);
+  };
+  auto tma_convert = [&](int k) {
+    mbar_wait(&s_mbar, tma_parity);
+    tma_parity ^= 1u;
+    if (cellw) convert_slot(k, ty + HY, tx + G);
+    constexpr int NXH = 2 * G * TY;
+    constexpr int NYH = 2 * G * TX;
+    for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {
+      if (h < NXH) {
+        const int r = h / (2 * G), w = h % (2 * G);
+        convert_slot(k, r + HY, (w < G) ? w : TX + w);
+      } else {
+        const int j = h - NXH, rs = j / TX, col = j % TX;
+        convert_slot(k, (rs < G) ? rs : TY + rs, col + G);
       }
     }
   };
@@ -363,6 +442,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // ------------------------------------------------------------------ march over z
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
+#ifdef MHD_WI_NOPF
+    if (false)
+#endif
     if (DIM == 3 && cellw) {
       // latency hiding, one iteration ahead: the own cell of plane k+G+1 (the z job's newest
       // plane next iteration) into L1 and of plane k+G+2 into L2; U^n of plane k (the update,
@@ -455,7 +537,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             q0[f] = Vc[(f * PH + ty + HY) * PW + tx + G];
             wl[f] = Vpz[f * NC + tid];
           }
+#ifdef MHD_WI_NOZCONV  // what-if (timing only): no re-conversion of the own column
+#pragma unroll
+          for (int f = 0; f < NV; ++f) q1[f] = q0[f];
+#else
           convert_own(k + 1, q1, false);
+#endif
           if constexpr (WZ) {  // cell k+1 from V(k-1..k+3); plane k+3 is first touched here
             double qm1[NV], q3[NV];
             convert_own(k - 1, qm1, false);
@@ -463,7 +550,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             convert_own(k + 3, q3, k + 3 >= kb && k + 3 < ke);
             fb = weno_cell<NV>(qm1, q0, q1, q2, q3, qp, qm);
           } else {  // cell k+1 from V(k..k+2); plane k+2 is first touched here
+#ifdef MHD_WI_NOZCONV
+#pragma unroll
+            for (int f = 0; f < NV; ++f) q2[f] = q0[f];
+#else
             convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
+#endif
             fb = plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
           }
           double wp[NV];
@@ -539,7 +631,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     }
     if (!full) {  // 3D prologue iteration: bring plane kb into Vc
       __syncthreads();
-      load_plane(kb, false);
+      if (tma) {
+        tma_issue(kb);
+        tma_convert(kb);
+      } else {
+        load_plane(kb, false);
+      }
       __syncthreads();
       continue;
     }
@@ -552,8 +649,14 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     // at the top of the iteration).
     __syncthreads();
     if constexpr (DIM == 3) {
-      if (k + 1 < ke) load_plane(k + 1, false);
+      if (k + 1 < ke) {
+        if (tma) tma_issue(k + 1);
+        else load_plane(k + 1, false);
+      }
     }
+#ifdef MHD_WI_NOUPD  // what-if (timing only): no update
+    if (false)
+#endif
     if (own) {  // (own: the cell is not wrapped, own_cell = gy * nx + gx)
       const size_t off = (size_t)a.gz * pstride + own_cell;
       const double* pu = opaque(at(a.Uin + off, k));
@@ -581,7 +684,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       }
     }
     if constexpr (DIM == 3) {
-      if (k + 1 < ke) __syncthreads();
+      if (k + 1 < ke) {
+        if (tma) tma_convert(k + 1);  // (after the update: the copy flew while it ran)
+        __syncthreads();
+      }
     }
   }
   __syncthreads();
@@ -753,14 +859,57 @@ cudaError_t launch_fast_ops(const double* A, const double* B, long long n, doubl
 // ---------------------------------------------------------------------------------------
 // host-side launchers (explicit instantiations)
 // ---------------------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3D: the TMA descriptor of the stage input — a 4D fp64 tensor (x, y, field, storage plane) with
+// the plane window of a tile (PW x PH x NV x 1) as its box.  TMA needs 16-byte row strides (nx
+// even); otherwise, or with MHD_NO_TMA=1, the kernel loads the window with per-thread loads.
+template <int NV>
+static int encode_window_map(StageArgs& a, int PW, int PH) {
+  static const bool off = [] { const char* e = getenv("MHD_NO_TMA"); return e && atoi(e) == 1; }();
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (off || !enc || (a.nx & 1)) return 0;
+  const cuuint64_t dims[4] = {(cuuint64_t)a.nx, (cuuint64_t)a.ny, (cuuint64_t)NV, (cuuint64_t)(a.nz_loc + 2 * a.gz)};
+  const cuuint64_t row = (cuuint64_t)a.nx * sizeof(double);
+  const cuuint64_t strides[3] = {row, row * (cuuint64_t)a.ny, row * (cuuint64_t)a.ny * NV};
+  const cuuint32_t box[4] = {(cuuint32_t)PW, (cuuint32_t)PH, (cuuint32_t)NV, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.Uin), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
+// the TMA plane window is used by the 3D PLM kernels (the fused WENO-Z kernel, an A/B
+// alternative to the split stage, keeps per-thread loads)
+template <int DIM, int REC>
+constexpr bool stage_tma() { return DIM == 3 && REC != 2; }
+
 template <int DIM, int NV, int RS, int TY, int REC>
-static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
+static cudaError_t launch_stage_t(const StageArgs& a0, cudaStream_t st) {
   using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
-  auto kern = k_stage<DIM, NV, RS, TY, REC>;
+  constexpr bool T = stage_tma<DIM, REC>();
+  auto kt = k_stage<DIM, NV, RS, TY, REC, T>;
+  auto kp = k_stage<DIM, NV, RS, TY, REC, false>;
+  if (a0.ze <= a0.zb) return cudaSuccess;
+  StageArgs a = a0;
+  a.tma = T ? encode_window_map<NV>(a, S::PW, S::PH) : 0;
+  auto kern = a.tma ? kt : kp;
   // (the attribute is per device: set on every launch, a host-side call of ~1 us)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   if (e != cudaSuccess) return e;
-  if (a.ze <= a.zb) return cudaSuccess;
   dim3 grid((a.nx + 31) / 32, (a.ny + TY - 1) / TY, (a.ze - a.zb + a.kz - 1) / a.kz);
   kern<<<grid, S::NT, S::bytes, st>>>(a);
   return cudaGetLastError();
@@ -808,7 +957,7 @@ int stage_tile_rows(int dim, int limiter) {
 template <int DIM, int NV, int RS, int TY, int REC>
 static int ctas_per_sm_t() {
   using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
-  auto kern = k_stage<DIM, NV, RS, TY, REC>;
+  auto kern = k_stage<DIM, NV, RS, TY, REC, stage_tma<DIM, REC>()>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, S::NT, S::bytes) != cudaSuccess) n = 1;

@@ -1,5 +1,6 @@
 // mhd_kernels.h — internal interface between the host library (mhd_api.cu) and the kernels.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the type only: the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -11,6 +12,10 @@ namespace mhd {
 // Internal state layout: [z + gz][f][y][x], x fastest, x/y unpadded (ghosts
 // resolved by index wrap/clamp), gz = 2 ghost planes per side in 3D (0 otherwise).
 struct StageArgs {
+  // 3D: TMA descriptor of Uin as the 4D tensor [storage plane][field][y][x] (fp64, no swizzle),
+  // box = one plane window of the CTA's tile with its x/y halo; set by launch_stage (tma = 1)
+  alignas(64) CUtensorMap tmap;
+  int tma;
   const double* Uin;  // stage input, read with the stencil
   const double* Un;   // stage 2: U^n, read pointwise (aliases Uout)
   double* Uout;       // stage 1: U*, stage 2: U^n (in place)

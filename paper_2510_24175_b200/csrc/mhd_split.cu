@@ -172,12 +172,15 @@ __global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_m(SplitArgs a) {
   if (hlls) atomicAdd(a.counters + 2, (unsigned long long)hlls);
 }
 
-// x faces i in [0, nx] of the rows (j, k): warps over the 32-cell chunks of [0, nx), q+ of cell
-// i-1 from lane l-1; the faces at chunk starts and the last face nx in a second pass, one per thread
+// x faces i in [0, nx] of the rows (j, k).  A warp item covers the 32 cells 31t-1 .. 31t+30 of a
+// row: every lane reconstructs its cell once; lanes 1..31 solve the faces i-1/2 with q+ of cell
+// i-1 from lane l-1 (a shuffle).  Items overlap by one cell, so the faces at item starts need no
+// second pass (the lane-0 cell is reconstructed twice: 1/32 of the work) and every read is a
+// coalesced row segment that the neighbouring items also touch (L1/L2 hits, V read once from HBM).
 template <int RS>
 __global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_x(SplitArgs a) {
   const SpIdx X = make_idx(a);
-  const int nf = a.nx, nch = (nf + 31) / 32;
+  const int nf = a.nx + 1, nch = (nf + 30) / 31;  // faces per row, items per row
   const size_t items = (size_t)nch * a.ny * a.nz;
   const int lane = threadIdx.x & 31;
   const size_t gw = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
@@ -187,28 +190,15 @@ __global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_x(SplitArgs a) {
     const int cx = (int)(w % nch);
     const size_t row = w / nch;
     const int j = (int)(row % a.ny), k = (int)(row / a.ny);
-    const int i = cx * 32 + lane;  // (i >= nx: a duplicate, never stored)
+    const int i = cx * 31 - 1 + lane;  // (i < 0 or i > nx: the wrapped / clamped cell; i >= nx never counted)
     double qp[NVS], qm[NVS], pl[NVS];
     const bool fb = sp_recon<0>(a, X, i, j, k, qp, qm);
 #pragma unroll
     for (int f = 0; f < NVS; ++f) pl[f] = __shfl_up_sync(0xffffffffu, qp[f], 1);
-    if (lane > 0 && i < nf) {
+    if (lane > 0 && i <= a.nx) {  // face i-1/2, i in [0, nx]
       fbs += (fb && i < a.nx) ? 1 : 0;
       hlls += sp_solve_store<0, RS>(a, pl, qm, i, j, k) ? 1 : 0;
     }
-  }
-  const size_t nt = (size_t)gridDim.x * blockDim.x;
-  const size_t items2 = (size_t)(nch + 1) * a.ny * a.nz;
-  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < items2; q += nt) {  // chunk starts, face nx
-    const int cx = (int)(q % (nch + 1));
-    const size_t row = q / (nch + 1);
-    const int j = (int)(row % a.ny), k = (int)(row / a.ny);
-    const int i = cx < nch ? cx * 32 : a.nx;
-    double pl[NVS], qm[NVS], t[NVS];
-    sp_recon<0>(a, X, i - 1, j, k, pl, t);
-    const bool fb = sp_recon<0>(a, X, i, j, k, t, qm);
-    fbs += (fb && i < a.nx) ? 1 : 0;
-    hlls += sp_solve_store<0, RS>(a, pl, qm, i, j, k) ? 1 : 0;
   }
   if (fbs) atomicAdd(a.counters + 1, (unsigned long long)fbs);
   if (hlls) atomicAdd(a.counters + 2, (unsigned long long)hlls);
@@ -253,7 +243,7 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
   };
   const size_t segy = (size_t)a.nx * a.nz * ((a.ny + 1 + kSpSeg - 1) / kSpSeg);
   const size_t segz = (size_t)a.nx * a.ny * ((a.nz + 1 + kSpSeg - 1) / kSpSeg);
-  const size_t xw = (size_t)((a.nx + 31) / 32) * 32 * a.ny * a.nz;
+  const size_t xw = (size_t)((a.nx + 1 + 30) / 31) * 32 * a.ny * a.nz;
   k_sp_prim<<<grid(pc * (a.nz + 6), 256, 16), 256, 0, st>>>(a);
   // the three face kernels are independent (V in, their own F out): y and z on two auxiliary
   // streams, joined before the update, so one kernel's tail overlaps the others
