@@ -284,17 +284,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   const size_t pstride = (size_t)fs * NV;
   const int kb = a.zb + blockIdx.z * a.kz;  // this CTA's z chunk inside [zb, ze)
   const int ke = min(kb + a.kz, a.ze);
-#ifdef MHD_STAGGER_NS
-  // measurement only: the second half of the grid starts later (de-phases co-resident CTAs)
-  if ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x >= gridDim.x * gridDim.y * gridDim.z / 2)
-    __nanosleep(MHD_STAGGER_NS);
-#endif
   // rare events (floors, fallbacks, HLL fallbacks, bad cells) go to shared-memory counters by
   // atomics only when they happen: no registers held for them across the face solves
   __shared__ int s_cnt[3];
   __shared__ unsigned long long s_bad;
   __shared__ uint64_t s_mbar;  // TMA plane-window completion
   constexpr bool tma = DIM == 3 && TMA;  // the plane window by TMA (a.tmap) instead of per-thread loads
+
   uint32_t tma_parity = 0;
   if (tid == 0) {
     s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
@@ -347,9 +343,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     }
     constexpr int NXH = 2 * G * TY;
     constexpr int NYH = (DIM >= 2) ? 2 * G * TX : 0;
-#ifdef MHD_WI_NOHALO  // what-if (timing only): the halo keeps the previous plane
-    if (false)
-#endif
     for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {  // the edge warp takes the first slots
       double v[NV];
       if (h < NXH) {
@@ -442,9 +435,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // ------------------------------------------------------------------ march over z
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
-#ifdef MHD_WI_NOPF
-    if (false)
-#endif
     if (DIM == 3 && cellw) {
       // latency hiding, one iteration ahead: the own cell of plane k+G+1 (the z job's newest
       // plane next iteration) into L1 and of plane k+G+2 into L2; U^n of plane k (the update,
@@ -537,12 +527,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             q0[f] = Vc[(f * PH + ty + HY) * PW + tx + G];
             wl[f] = Vpz[f * NC + tid];
           }
-#ifdef MHD_WI_NOZCONV  // what-if (timing only): no re-conversion of the own column
-#pragma unroll
-          for (int f = 0; f < NV; ++f) q1[f] = q0[f];
-#else
           convert_own(k + 1, q1, false);
-#endif
           if constexpr (WZ) {  // cell k+1 from V(k-1..k+3); plane k+3 is first touched here
             double qm1[NV], q3[NV];
             convert_own(k - 1, qm1, false);
@@ -550,12 +535,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             convert_own(k + 3, q3, k + 3 >= kb && k + 3 < ke);
             fb = weno_cell<NV>(qm1, q0, q1, q2, q3, qp, qm);
           } else {  // cell k+1 from V(k..k+2); plane k+2 is first touched here
-#ifdef MHD_WI_NOZCONV
-#pragma unroll
-            for (int f = 0; f < NV; ++f) q2[f] = q0[f];
-#else
             convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
-#endif
             fb = plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
           }
           double wp[NV];
@@ -654,9 +634,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         else load_plane(k + 1, false);
       }
     }
-#ifdef MHD_WI_NOUPD  // what-if (timing only): no update
-    if (false)
-#endif
     if (own) {  // (own: the cell is not wrapped, own_cell = gy * nx + gx)
       const size_t off = (size_t)a.gz * pstride + own_cell;
       const double* pu = opaque(at(a.Uin + off, k));
