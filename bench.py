@@ -412,7 +412,8 @@ def main():
 
     # ---- timed region (device time, CUDA events on the library's stream = torch's current stream)
     nst = 3 if p.stepper else 2
-    s.profile_enable(True, capacity=args.steps * (nst + 1) + 8)  # one event pair per stage and per dt pass
+    # one event pair per stage and per dt pass, and per stage one for the exposed halo wait (slabs)
+    s.profile_enable(True, capacity=args.steps * (2 * nst + 1) + 8)
     with ClockSampler(local_rank) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -472,6 +473,7 @@ def main():
             "cells_per_launch": cells_loc, "stage_ms_per_launch": stage_avg_s * 1e3, "stage_launches": stage_n,
             "stage_share_of_step": stage_ms / max(ms, 1e-9),
             "dt_ms_per_launch": prof["dt"][0] / max(prof["dt"][1], 1),
+            "halo_exposed_ms_per_step": prof["halo_exposed"][0] / args.steps,
             "fp64_pipe_active_pct": (sum(c["fp64_pipe_active_pct"] for c in caps) / nst) if all(caps) else None,
             "per_stage": per_stage,
             "hbm": {"achieved": by_avg * cells_loc / stage_avg_s / 1e9 if by_avg else None, "peak": hbm_peak,

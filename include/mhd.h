@@ -243,8 +243,11 @@ int mhd_debug_face_flux(mhd_ctx* ctx, const double* VL, const double* VR, int64_
 int mhd_profile_enable(mhd_ctx* ctx, int32_t enable);
 int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
 /* The same totals per class: index 0 the dt pass, 1..3 RK stage 1..3 (RK2 leaves 3 at zero),
- * so per-stage rooflines can be formed (stage 1 and stage 2 move different bytes). */
-int mhd_profile_read_stages(mhd_ctx* ctx, double ms[4], int64_t units[4]);
+ * so per-stage rooflines can be formed (stage 1 and stage 2 move different bytes); index 4 the
+ * exposed halo wait of slab runs (per stage: from the end of the interior launch to the halo's
+ * completion on the compute stream — the exchange time the interior did not hide; zero on one
+ * slab).  The stage intervals include their halo wait. */
+int mhd_profile_read_stages(mhd_ctx* ctx, double ms[5], int64_t units[5]);
 
 /* Library build identity, e.g. "libmhd sm_100a fused-v1". */
 const char* mhd_version(void);

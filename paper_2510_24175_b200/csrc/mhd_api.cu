@@ -12,6 +12,7 @@
 // in-process slab group (decomposition tests on one GPU) and kernel timing.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost a pointer test unless a tool is attached
 
 #include <cmath>
 #include <cstdarg>
@@ -87,8 +88,10 @@ struct mhd_ctx {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> ev_kind;  // one entry per recorded (start, stop) pair: its class
-  double prof_ms[4] = {0, 0, 0, 0};  // per timed class: 0 dt pass, 1..3 RK stage
-  int64_t prof_n[4] = {0, 0, 0, 0};
+  // per timed class: 0 dt pass, 1..3 RK stage, 4 exposed halo wait (slabs: the compute stream's
+  // wait for the halo after the interior launch)
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+  int64_t prof_n[5] = {0, 0, 0, 0, 0};
   int64_t prof_dropped = 0;
   size_t prof_cap = 0;  // pairs the pool has room for (mhd_profile_enable)
 };
@@ -397,21 +400,31 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
 int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
+  nvtxRangePushA(stage == 1 ? "mhd stage 1" : stage == 2 ? "mhd stage 2" : "mhd stage 3");
   if (c->nranks > 1 && c->dim == 3) {
-    if ((rc = exchange(c, stage))) return rc;
+    nvtxRangePushA("mhd halo exchange");
+    rc = exchange(c, stage);
+    nvtxRangePop();
+    if (rc) return rc;
     const int pr = prof_begin(c, stage);
     const int g = c->gz;
     const int lo = g < c->nzl ? g : c->nzl, hi = c->nzl - g > lo ? c->nzl - g : lo;
     if ((rc = run_stage(c, stage, k, lo, hi))) return rc;
+    // class 4 brackets the wait: its start completes with the interior launch, its end when the
+    // halo has landed as well, so the pair measures the exchange time the interior did not hide
+    const int pw = prof_begin(c, 4);
     CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    prof_end(c, pw);
     if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
     if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
     prof_end(c, pr);
+    nvtxRangePop();
     return MHD_OK;
   }
   const int pr = prof_begin(c, stage);
   rc = run_stage(c, stage, k, 0, c->nzl);
   prof_end(c, pr);
+  nvtxRangePop();
   return rc;
 }
 
@@ -492,7 +505,14 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
 }
 
 // dt / c_h maxima of U^n into dbuf[0..1], reduced over ranks; reads back dbuf. Synchronising.
+int reduce_and_read_(mhd_ctx* c);
 int reduce_and_read(mhd_ctx* c) {
+  nvtxRangePushA("mhd dt (k_dt + allreduce + read-back)");
+  const int rc = reduce_and_read_(c);
+  nvtxRangePop();
+  return rc;
+}
+int reduce_and_read_(mhd_ctx* c) {
   CUDA_OR_RETURN(c, cudaMemsetAsync(c->dbuf, 0, 2 * sizeof(unsigned long long), c->stream));
   DtArgs d;
   d.U = c->U0;
@@ -1221,7 +1241,7 @@ int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
   }
   c->prof_cap = pairs;
   c->ev_kind.clear();
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 5; ++i) {
     c->prof_ms[i] = 0.0;
     c->prof_n[i] = 0;
   }
@@ -1229,10 +1249,10 @@ int mhd_profile_enable(mhd_ctx* c, int32_t enable) {
   return MHD_OK;
 }
 
-int mhd_profile_read_stages(mhd_ctx* c, double ms[4], int64_t units[4]) {
+int mhd_profile_read_stages(mhd_ctx* c, double ms[5], int64_t units[5]) {
   if (!c || !ms || !units) return MHD_E_ARG;
   prof_drain(c);
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 5; ++i) {
     ms[i] = c->prof_ms[i];
     units[i] = c->prof_n[i];
   }
@@ -1244,8 +1264,8 @@ int mhd_profile_read_stages(mhd_ctx* c, double ms[4], int64_t units[4]) {
 
 int mhd_profile_read(mhd_ctx* c, double ms[2], int64_t launches[2]) {
   if (!c || !ms || !launches) return MHD_E_ARG;
-  double m4[4];
-  int64_t n4[4];
+  double m4[5];
+  int64_t n4[5];
   const int rc = mhd_profile_read_stages(c, m4, n4);
   ms[0] = m4[1] + m4[2] + m4[3];
   launches[0] = n4[1] + n4[2] + n4[3];

@@ -308,10 +308,12 @@ class Solver:
         return {"stage": (ms[0], n[0]), "dt": (ms[1], n[1])}
 
     def profile_read_stages(self):
-        """{'dt': (ms, passes), 'stage1': (ms, stages), 'stage2': ..., 'stage3': ...} since profile_enable."""
-        ms, n = (C.c_double * 4)(), (C.c_int64 * 4)()
+        """{'dt': (ms, passes), 'stage1': (ms, stages), 'stage2': ..., 'stage3': ..., 'halo_exposed':
+        (ms, waits)} since profile_enable."""
+        ms, n = (C.c_double * 5)(), (C.c_int64 * 5)()
         self._check(self._L.mhd_profile_read_stages(self._h, ms, n))
-        return {"dt": (ms[0], n[0]), "stage1": (ms[1], n[1]), "stage2": (ms[2], n[2]), "stage3": (ms[3], n[3])}
+        return {"dt": (ms[0], n[0]), "stage1": (ms[1], n[1]), "stage2": (ms[2], n[2]), "stage3": (ms[3], n[3]),
+                "halo_exposed": (ms[4], n[4])}
 
     def destroy(self) -> None:
         if getattr(self, "_h", None):

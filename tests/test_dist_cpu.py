@@ -167,3 +167,18 @@ def test_halo_plan_all_rank_counts(world, ghost, periodic):
                     assert np.array_equal(S[r][sp], G[zg % nz_glob]), (r, sp, zg)
                 elif world > 1:
                     assert np.isnan(S[r][sp]).all()
+
+
+def test_nccl_bench_script_runs_on_gloo(tmp_path):
+    """tools/nccl_bench.py's halo / allreduce schedule, run with the gloo backend on 2 CPU ranks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29541",
+                        os.path.join(root, "tools", "nccl_bench.py"), "--backend", "gloo", "--sizes", "32", "--iters", "3",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["world"] == 2 and d["halo"][0]["message_MB"] == 2 * 9 * 32 * 32 * 8 / 1e6 and d["allreduce_16B"]["us"] > 0

@@ -995,3 +995,28 @@ def test_nccl_two_ranks_bitwise(mhd, tmp_path):
     import json
     res = json.loads(out.read_text())
     assert all(r["bitwise"] for r in res["cases"]), res
+
+
+def test_profile_exposed_halo_class_on_slabs(mhd):
+    """Slabs record, per stage, the compute stream's wait for the halo after the interior launch
+    (mhd_profile_read_stages class 4); one slab records none."""
+    p = I.orszag_tang_3d(32)
+    U0 = I.orszag_tang_3d_ic(p)
+    g = mhd.SolverGroup(p, 4)
+    g.set_state(U0)
+    g.run(1)
+    for s in g.slabs:
+        s.profile_enable(True, capacity=64)
+    g.run(3)
+    for s in g.slabs:
+        pr = s.profile_read_stages()
+        assert pr["halo_exposed"][1] == 6 and pr["halo_exposed"][0] >= 0.0
+        assert pr["stage1"][1] == 3 and pr["stage2"][1] == 3 and pr["dt"][1] == 3
+        assert pr["halo_exposed"][0] <= pr["stage1"][0] + pr["stage2"][0]
+    g.destroy()
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    s.profile_enable(True)
+    s.run(2)
+    assert s.profile_read_stages()["halo_exposed"] == (0.0, 0)
+    s.destroy()
