@@ -124,7 +124,7 @@ template <int D, int RS>
 __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* vl, const double* vr, int i, int j,
                                               int k) {
   double fn[NVS], fx[NVS];
-  const int fell = face_flux<NVS, RS>(vl, vr, a.c, fn);
+  const int fell = face_flux<NVS, RS, true>(vl, vr, a.c, fn);
   from_normal<NVS, D>(fn, fx);
   double* F = a.F[D] + fidx(a, 0, i, j, k);
   asm("mov.b64 %0, %0;" : "+l"(F));

@@ -28,8 +28,19 @@ def main():
     from paper_2510_24175_b200 import mhd
     p = I.orszag_tang_3d(args.n)
     U0 = I.workload_ic("ot3d", p, 0, p.n[2])
+    s1 = mhd.Solver(p, stream=torch.cuda.current_stream())  # P = 1 reference: one slab, no halo
+    s1.set_state(U0)
+    s1.run(2)
+    s1.profile_enable(True, capacity=args.steps * 5 + 8)
+    s1.run(args.steps)
+    pr = s1.profile_read_stages()
+    print(json.dumps({"n": args.n, "P": 1, "steps": args.steps,
+                      "stage_ms_per_step_sum_over_slabs": (pr["stage1"][0] + pr["stage2"][0]) / args.steps,
+                      "halo_exposed_ms_per_step_sum_over_slabs": 0.0}), flush=True)
+    s1.destroy()
     for P in args.P:
         g = mhd.SolverGroup(p, P)
+        g.slabs[0].set_stream(torch.cuda.current_stream())  # the group runs on slab 0's stream
         g.set_state(U0)
         g.run(2)
         for s in g.slabs:
