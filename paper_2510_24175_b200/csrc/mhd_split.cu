@@ -134,7 +134,10 @@ __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* 
   return fell;
 }
 
-constexpr int kSpSeg = 16;  // faces per marching segment (at most; segments of a line are balanced)
+#ifndef MHD_SP_SEG
+#define MHD_SP_SEG 16
+#endif
+constexpr int kSpSeg = MHD_SP_SEG;  // faces per marching segment (at most; segments of a line are balanced)
 #ifndef MHD_SP_MINB
 #define MHD_SP_MINB 3  // 3 blocks of 128 per SM (<= 168 registers): +2% over no bound, 4 spills more
 #endif
