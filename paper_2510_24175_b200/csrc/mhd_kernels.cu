@@ -213,6 +213,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
 
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
+#ifndef MHD_EDGE_HALO
+#define MHD_EDGE_HALO 1
+#endif
+constexpr int kEdgeHalo = MHD_EDGE_HALO;  // TMA window: halo slots converted per edge-warp thread
 #ifndef MHD_JOB_UNROLL
 #define MHD_JOB_UNROLL 1
 #endif
@@ -387,7 +391,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     if (cellw) convert_slot(k, ty + HY, tx + G);
     constexpr int NXH = 2 * G * TY;
     constexpr int NYH = 2 * G * TX;
-    for (int h = (tid + 32) % NT; h < NXH + NYH; h += NT) {
+    // halo slots: the edge warp (no update, no own cell) takes the first 32 * kEdgeHalo, the cell
+    // threads the rest
+    constexpr int E = 32 * kEdgeHalo < NXH + NYH ? 32 * kEdgeHalo : NXH + NYH;
+    auto slot = [&](int h) {
       if (h < NXH) {
         const int r = h / (2 * G), w = h % (2 * G);
         convert_slot(k, r + HY, (w < G) ? w : TX + w);
@@ -395,6 +402,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         const int j = h - NXH, rs = j / TX, col = j % TX;
         convert_slot(k, (rs < G) ? rs : TY + rs, col + G);
       }
+    };
+    if (!cellw) {
+#pragma unroll 1
+      for (int h = tid - NC; h < E; h += 32) slot(h);
+    } else {
+#pragma unroll 1
+      for (int h = E + tid; h < NXH + NYH; h += NC) slot(h);
     }
   };
 
