@@ -560,7 +560,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
 
   /* validity of the stage input (R16): lowest interior linear index */
   int64_t first_bad = INT64_MAX;
-#pragma omp parallel for reduction(min : first_bad) schedule(static)
+#pragma omp parallel for collapse(2) reduction(min : first_bad) schedule(static)
   for (int64_t k = 0; k < G->n[2]; ++k)
     for (int64_t j = 0; j < G->n[1]; ++j)
       for (int64_t i = 0; i < G->n[0]; ++i) {
@@ -579,7 +579,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
   /* c.3 on every cell the star stencil touches */
   double* V = (double*)calloc(np, sizeof(double));
   int64_t floors = 0;
-#pragma omp parallel for reduction(+ : floors) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : floors) schedule(static)
   for (int64_t k = -G->g[2]; k < G->n[2] + G->g[2]; ++k)
     for (int64_t j = -G->g[1]; j < G->n[1] + G->g[1]; ++j)
       for (int64_t i = -G->g[0]; i < G->n[0] + G->g[0]; ++i) {
@@ -606,7 +606,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
     int64_t lo3[3] = {0, 0, 0}, hi3[3] = {G->n[0], G->n[1], G->n[2]};
     lo3[d] = -1;
     hi3[d] = G->n[d] + 1;
-#pragma omp parallel for reduction(+ : fallbacks) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : fallbacks) schedule(static)
     for (int64_t k = lo3[2]; k < hi3[2]; ++k)
       for (int64_t j = lo3[1]; j < hi3[1]; ++j)
         for (int64_t i = lo3[0]; i < hi3[0]; ++i) {
@@ -641,7 +641,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
     /* faces i-1/2 for i = 0..N: VL = V+[i-1], VR = V-[i] */
     int64_t fhi[3] = {G->n[0], G->n[1], G->n[2]};
     fhi[d] = G->n[d] + 1;
-#pragma omp parallel for reduction(+ : to_hll) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : to_hll) schedule(static)
     for (int64_t k = 0; k < fhi[2]; ++k)
       for (int64_t j = 0; j < fhi[1]; ++j)
         for (int64_t i = 0; i < fhi[0]; ++i) {
@@ -661,7 +661,7 @@ static int stage_op(const orc_config* c, const grid_t* G, double* Up, double* Ou
   cnt->hlld_to_hll += to_hll;
 
   /* c.11 update: r = lx dFx; r = r + ly dFy; r = r + lz dFz; S(U) = U - r */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for collapse(2) schedule(static)
   for (int64_t k = 0; k < G->n[2]; ++k)
     for (int64_t j = 0; j < G->n[1]; ++j)
       for (int64_t i = 0; i < G->n[0]; ++i)
@@ -790,7 +790,7 @@ static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, 
   /* 1-2: cell-centred primitives */
   double* V = (double*)calloc(8 * ncell, sizeof(double));
   int64_t floors = 0;
-#pragma omp parallel for reduction(+ : floors) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : floors) schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -810,7 +810,7 @@ static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, 
     double* Vm = (double*)calloc(8 * ncell, sizeof(double));
     int64_t o[3] = {0, 0, 0};
     o[d] = 1;
-#pragma omp parallel for reduction(+ : fallbacks) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : fallbacks) schedule(static)
     for (int64_t k = 0; k < nz; ++k)
       for (int64_t j = 0; j < ny; ++j)
         for (int64_t i = 0; i < nx; ++i) {
@@ -840,7 +840,7 @@ static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, 
             Vm[ct_at(G, f, i, j, k)] = qm[f];
           }
         }
-#pragma omp parallel for reduction(+ : to_hll) schedule(static)
+#pragma omp parallel for collapse(2) reduction(+ : to_hll) schedule(static)
     for (int64_t k = 0; k < nz; ++k)
       for (int64_t j = 0; j < ny; ++j)
         for (int64_t i = 0; i < nx; ++i) {
@@ -869,7 +869,7 @@ static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, 
   double* Ez = (double*)calloc(ncell, sizeof(double));
   double* Ex = (double*)calloc(ncell, sizeof(double));
   double* Ey = (double*)calloc(ncell, sizeof(double));
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for collapse(2) schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -889,7 +889,7 @@ static int stage_op_ct(const orc_config* c, const grid_t* G, const double* Uin, 
       }
 
   /* 6: update */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for collapse(2) schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -1030,7 +1030,7 @@ int orc_compute_dt(const orc_config* c, const double* U, double* dt, double* ch,
   const size_t ncell = (size_t)G.n[0] * G.n[1] * G.n[2];
   double M = 0.0, S = 0.0;
   int64_t first_bad = INT64_MAX;
-#pragma omp parallel for reduction(max : M, S) reduction(min : first_bad) schedule(static)
+#pragma omp parallel for collapse(2) reduction(max : M, S) reduction(min : first_bad) schedule(static)
   for (int64_t k = 0; k < G.n[2]; ++k)
     for (int64_t j = 0; j < G.n[1]; ++j)
       for (int64_t i = 0; i < G.n[0]; ++i) {
