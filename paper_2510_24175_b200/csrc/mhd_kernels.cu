@@ -320,14 +320,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   auto convert_own = [&](int k, double* v, bool count) {
     double u[NV];
     load_fields<NV>(at(Ucol, k), fs, u);
-#ifdef MHD_WI_VARR  // what-if (timing only): the stored state is already primitive
-#pragma unroll
-    for (int f = 0; f < NV; ++f) v[f] = u[f];
-    const bool fl = v[4] < c.p_floor;
-    v[4] = fl ? c.p_floor : v[4];
-#else
     const bool fl = cons2prim<NV>(u, v, c.gm1, c.p_floor);
-#endif
     if (count && own) {
       if (fl) atomicAdd(&s_cnt[0], 1);
       if (bad_state<NV>(u)) atomicMin(&s_bad, glin(k));
@@ -383,9 +376,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
     const int x = x0 + col - G, y = y0 + r - HY;
     double v[NV];
     if (x >= 0 && x < nx && y >= 0 && y < ny) {
-#ifdef MHD_WI_VARR
-      return;
-#endif
       double u[NV];
 #pragma unroll
       for (int f = 0; f < NV; ++f) u[f] = Vc[(f * PH + r) * PW + col];
