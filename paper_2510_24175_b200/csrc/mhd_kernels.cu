@@ -213,6 +213,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
 
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
+#ifndef MHD_ZTMA
+#define MHD_ZTMA 1
+#endif
 #ifndef MHD_EDGE_HALO
 #define MHD_EDGE_HALO 1
 #endif
@@ -235,9 +238,13 @@ struct StageSmem {
   static constexpr int nVc = NV * PH * PW;
   static constexpr int nCol = (DIM == 3) ? NV * TY * TX : 0;  // Vpz, Fz[0], Fz[1] each
   static constexpr int nFy = (DIM >= 2) ? NV * (TY + 1) * TX : 0;
-  static constexpr int nFx = NV * TY * (TX + 1);
+  static constexpr int FXP = TX + 2;  // x-flux row pitch (16-byte rows: a TMA box can fill it)
+  static constexpr int nFx = NV * TY * FXP;
   static constexpr int nXP = NV * TY;  // q+ (x) of cell x0-1 per row, from the edge warp
-  static constexpr size_t bytes = sizeof(double) * (size_t)(nVc + 3 * nCol + nFy + nFx + nXP);
+  // Fy and Fx start on 128-byte boundaries (TMA destinations of the z staging, MHD_ZTMA)
+  static constexpr int oFy = (nVc + 3 * nCol + 15) / 16 * 16;
+  static constexpr int oFx = (oFy + nFy + 15) / 16 * 16;
+  static constexpr size_t bytes = sizeof(double) * (size_t)(oFx + nFx + nXP);
 };
 
 #ifndef MHD_OCCW
@@ -273,8 +280,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   double* Vc = smem;                 // [NV][PH][PW] primitives of plane k (+halo); TMA destination
   double* Vpz = Vc + S::nVc;         // [NV][NC] V+ (z normal frame) of plane k   (3D)
   double* Fz = Vpz + S::nCol;        // [2][NV][NC] z fluxes, face k+1/2 in Fz[(k+1)&1] (3D)
-  double* Fy = Fz + 2 * S::nCol;     // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
-  double* Fx = Fy + S::nFy;          // [NV][TY][TX+1] x-face fluxes of plane k
+  double* Fy = smem + S::oFy;        // [NV][TY+1][TX] y-face fluxes of plane k (2D/3D)
+  double* Fx = smem + S::oFx;        // [NV][TY][FXP] x-face fluxes of plane k
   double* XP = Fx + S::nFx;          // [NV][TY] q+ along x of cell x0-1 of every row
 
   const StageConsts& c = a.c;
@@ -293,13 +300,23 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   __shared__ int s_cnt[3];
   __shared__ unsigned long long s_bad;
   __shared__ uint64_t s_mbar;  // TMA plane-window completion
+  __shared__ uint64_t s_mbar2;  // TMA z-staging completion (ZT)
   constexpr bool tma = DIM == 3 && TMA;  // the plane window by TMA (a.tmap) instead of per-thread loads
+  // ZT: the own-cell tiles of planes k+1 and k+2 for the z job of iteration k are staged by TMA
+  // in the y- and x-flux buffers, which are dead from the end of the previous update (the
+  // window barrier) to this plane's y and x jobs (each warp's flux writes cover exactly its own
+  // staged rows, which its z job has already read); issued at the top of the iteration.  Same
+  // time as the per-thread loads it replaces (3.43 ms; issued after the update behind one more
+  // barrier instead: 3.60 ms)
+  constexpr bool ZT = tma && !WZ && MHD_ZTMA;
+  uint32_t zt_parity = 0;
 
   uint32_t tma_parity = 0;
   if (tid == 0) {
     s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
     s_bad = ULLONG_MAX;
     if (tma) mbar_init(&s_mbar, 1);
+    if (ZT) mbar_init(&s_mbar2, 1);
   }
   __syncthreads();
 
@@ -371,6 +388,23 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   constexpr uint32_t kWinBytes = (uint32_t)(sizeof(double) * NV * PH * PW);
   auto tma_issue = [&](int k) {
     if (tid == 0) tma_load_window(Vc, &a.tmap, x0 - G, y0 - HY, a.gz + k, &s_mbar, kWinBytes);
+  };
+  constexpr uint32_t kFyBytes = (uint32_t)(sizeof(double) * NV * (TY + 1) * TX);
+  constexpr uint32_t kFxBytes = (uint32_t)(sizeof(double) * NV * TY * S::FXP);
+  auto zt_issue = [&](int kk) {  // raw U of planes kk (-> Fy) and kk + 1 (-> Fx), own tile
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_mbar2)),
+                   "r"(kFyBytes + kFxBytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+          ::"r"(smem_u32(Fy)), "l"(&a.tmap_fy), "r"(x0), "r"(y0), "r"(0), "r"(a.gz + kk), "r"(smem_u32(&s_mbar2))
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+          ::"r"(smem_u32(Fx)), "l"(&a.tmap_fx), "r"(x0), "r"(y0), "r"(0), "r"(a.gz + kk + 1), "r"(smem_u32(&s_mbar2))
+          : "memory");
+    }
   };
   auto convert_slot = [&](int k, int r, int col) {  // Vc slot (r, col): global (x0 + col - G, y0 + r - HY)
     const int x = x0 + col - G, y = y0 + r - HY;
@@ -449,6 +483,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
   // ------------------------------------------------------------------ march over z
   for (int k = kstart; k < ke; ++k) {
     const bool full = k >= kb;  // k = kb-1 (3D) only solves the z face kb-1/2
+    if (ZT && full) zt_issue(k + 1);  // (Fx, Fy are dead since the last update's barrier)
     if (DIM == 3 && cellw) {
       // latency hiding, one iteration ahead: the own cell of plane k+G+1 (the z job's newest
       // plane next iteration) into L1 and of plane k+G+2 into L2; U^n of plane k (the update,
@@ -541,7 +576,16 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             q0[f] = Vc[(f * PH + ty + HY) * PW + tx + G];
             wl[f] = Vpz[f * NC + tid];
           }
-          convert_own(k + 1, q1, false);
+          const bool staged = ZT && k != kstart;  // warp-uniform
+          if (staged) mbar_wait(&s_mbar2, zt_parity);
+          if (staged && own) {
+            double u[NV];
+#pragma unroll
+            for (int f = 0; f < NV; ++f) u[f] = Fy[(f * (TY + 1) + ty) * TX + tx];
+            cons2prim<NV>(u, q1, c.gm1, c.p_floor);
+          } else {
+            convert_own(k + 1, q1, false);
+          }
           if constexpr (WZ) {  // cell k+1 from V(k-1..k+3); plane k+3 is first touched here
             double qm1[NV], q3[NV];
             convert_own(k - 1, qm1, false);
@@ -549,7 +593,19 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
             convert_own(k + 3, q3, k + 3 >= kb && k + 3 < ke);
             fb = weno_cell<NV>(qm1, q0, q1, q2, q3, qp, qm);
           } else {  // cell k+1 from V(k..k+2); plane k+2 is first touched here
-            convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
+            if (staged && own) {
+              double u[NV];
+#pragma unroll
+              for (int f = 0; f < NV; ++f) u[f] = Fx[(f * TY + ty) * S::FXP + tx];
+              const bool fl = cons2prim<NV>(u, q2, c.gm1, c.p_floor);
+              if (k + 2 >= kb && k + 2 < ke) {  // the counted conversion of plane k+2 (convert_own's rule)
+                if (fl) atomicAdd(&s_cnt[0], 1);
+                if (bad_state<NV>(u)) atomicMin(&s_bad, glin(k + 2));
+              }
+            } else {
+              convert_own(k + 2, q2, k + 2 >= kb && k + 2 < ke);
+            }
+            if (staged) zt_parity ^= 1u;
             fb = plm_cell<NV, LIM>(q0, q1, q2, qp, qm);
           }
           double wp[NV];
@@ -620,7 +676,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         for (int f = 0; f < NV; ++f) Fy[(f * (TY + 1) + row) * TX + col] = fy[f];
       } else {
 #pragma unroll
-        for (int n = 0; n < NV; ++n) Fx[(n * TY + row) * (TX + 1) + col] = fn[n];
+        for (int n = 0; n < NV; ++n) Fx[(n * TY + row) * S::FXP + col] = fn[n];
       }
     }
     if (!full) {  // 3D prologue iteration: bring plane kb into Vc
@@ -663,7 +719,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       const double* fzo = Fz + (k & 1) * S::nCol;
 #pragma unroll
       for (int f = 0; f < NV; ++f) {
-        double r = c.lam[0] * (Fx[(f * TY + ty) * (TX + 1) + tx + 1] - Fx[(f * TY + ty) * (TX + 1) + tx]);
+        double r = c.lam[0] * (Fx[(f * TY + ty) * S::FXP + tx + 1] - Fx[(f * TY + ty) * S::FXP + tx]);
         if constexpr (DIM >= 2) r = r + c.lam[1] * (Fy[(f * (TY + 1) + ty + 1) * TX + tx] - Fy[(f * (TY + 1) + ty) * TX + tx]);
         if constexpr (DIM == 3) r = r + c.lam[2] * (fzn[f * NC + tid] - fzo[f * NC + tid]);
         const double s = u0[f] - r;
@@ -868,7 +924,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // the plane window of a tile (PW x PH x NV x 1) as its box.  TMA needs 16-byte row strides (nx
 // even); otherwise, or with MHD_NO_TMA=1, the kernel loads the window with per-thread loads.
 template <int NV>
-static int encode_window_map(StageArgs& a, int PW, int PH) {
+static int encode_window_map(StageArgs& a, int PW, int PH, int TYZ) {
   static const bool off = [] { const char* e = getenv("MHD_NO_TMA"); return e && atoi(e) == 1; }();
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (off || !enc || (a.nx & 1)) return 0;
@@ -877,10 +933,23 @@ static int encode_window_map(StageArgs& a, int PW, int PH) {
   const cuuint64_t strides[3] = {row, row * (cuuint64_t)a.ny, row * (cuuint64_t)a.ny * NV};
   const cuuint32_t box[4] = {(cuuint32_t)PW, (cuuint32_t)PH, (cuuint32_t)NV, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = enc(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.Uin), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 1 : 0;
+  CUresult r = enc(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.Uin), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return 0;
+  if (TYZ > 0) {  // the z-staging boxes: [f][TY+1][32] and [f][TY][34]
+    const cuuint32_t bfy[4] = {32, (cuuint32_t)(TYZ + 1), (cuuint32_t)NV, 1};
+    const cuuint32_t bfx[4] = {34, (cuuint32_t)TYZ, (cuuint32_t)NV, 1};
+    r = enc(&a.tmap_fy, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.Uin), dims, strides, bfy, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 0;
+    r = enc(&a.tmap_fx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.Uin), dims, strides, bfx, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 0;
+  }
+  return 1;
 }
 
 // the TMA plane window is used by the 3D PLM kernels (the fused WENO-Z kernel, an A/B
@@ -896,7 +965,7 @@ static cudaError_t launch_stage_t(const StageArgs& a0, cudaStream_t st) {
   auto kp = k_stage<DIM, NV, RS, TY, REC, false>;
   if (a0.ze <= a0.zb) return cudaSuccess;
   StageArgs a = a0;
-  a.tma = T ? encode_window_map<NV>(a, S::PW, S::PH) : 0;
+  a.tma = T ? encode_window_map<NV>(a, S::PW, S::PH, (MHD_ZTMA && REC != 2) ? TY : 0) : 0;
   auto kern = a.tma ? kt : kp;
   // (the attribute is per device: set on every launch, a host-side call of ~1 us)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);

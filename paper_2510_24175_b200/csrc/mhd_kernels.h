@@ -15,6 +15,10 @@ struct StageArgs {
   // 3D: TMA descriptor of Uin as the 4D tensor [storage plane][field][y][x] (fp64, no swizzle),
   // box = one plane window of the CTA's tile with its x/y halo; set by launch_stage (tma = 1)
   alignas(64) CUtensorMap tmap;
+  // 3D PLM (MHD_ZTMA): the own-cell tile of two planes for the next z job, boxes matching the
+  // y- and x-flux buffers they are staged in ([f][TY+1][32] and [f][TY][34])
+  alignas(64) CUtensorMap tmap_fy;
+  alignas(64) CUtensorMap tmap_fx;
   int tma;
   const double* Uin;  // stage input, read with the stencil
   const double* Un;   // stage 2: U^n, read pointwise (aliases Uout)
