@@ -266,15 +266,15 @@ def oracle_rate(ps, U, steps: int, warmup: int, threads: int = 0):
         oracle.set_num_threads(n0)
 
 
-def cpu_baseline(workload: str, p, scheme: str, steps: int = 2):
+def cpu_baseline(workload: str, p, scheme: str, steps: int = 6):
     """the oracle on all host cores (OMP_PROC_BIND=close, OMP_PLACES=cores) on
-    a ~4 M-cell slab of the workload, `steps` steps, and on one core on a 1/16 slab; ~10-30 s"""
+    a ~4 M-cell slab of the workload, `steps` steps, and on one core on a 1/8 slab; ~10-20 s"""
     model, sockets, cps, tpc = cpu_topology()
     n2 = p.n[0] * p.n[1]
     nz_all = max(4, min(p.n[2], (4 << 20) // n2))
     ps, U = oracle_slab(workload, p, nz_all)
     v_all, el_all, cores = oracle_rate(ps, U, steps, 0)
-    nz_one = max(4, nz_all // 16)
+    nz_one = max(4, nz_all // 8)
     ps1, U1 = oracle_slab(workload, p, nz_one)
     v_one, el_one, _ = oracle_rate(ps1, U1, 1, 0, threads=1)
     return {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model, "sockets": sockets,
