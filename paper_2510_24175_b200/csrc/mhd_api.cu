@@ -64,6 +64,10 @@ struct mhd_ctx {
   bool own_stream = false;
   ncclComm_t comm = nullptr;
   int transport = MHD_TRANSPORT_NCCL;
+  // MHD_NCCL_SELF=1 (test/validation): one periodic 3D rank runs the slab schedule with its
+  // z ghost planes exchanged through a one-rank NCCL communicator (send/recv to itself) and the
+  // dt reduction through ncclAllReduce — the NCCL code path of the multi-GPU run, on one GPU
+  bool nccl_self = false;
   cudaStream_t comm_stream = nullptr;            // NCCL halo exchange (overlaps the interior)
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   mhd_ctx* const* group = nullptr;                // MHD_TRANSPORT_LOCAL: the slabs of this group
@@ -125,13 +129,20 @@ int set_err(mhd_ctx* c, int code, const char* fmt, ...) {
 
 size_t plane_elems(const mhd_ctx* c) { return (size_t)c->nv * c->nx * c->ny; }
 
+// the context runs the slab schedule (a z halo exchange per stage): slabs, or the NCCL self test
+bool slabbed(const mhd_ctx* c) { return c->nranks > 1 || c->nccl_self; }
+// its halo and reductions go through an NCCL communicator
+bool nccl_active(const mhd_ctx* c) {
+  return c->comm && ((c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) || c->nccl_self);
+}
+
 // Host wait for the context's stream.  With NCCL slabs the stream may wait on collectives of
 // the other ranks: poll it together with ncclCommGetAsyncError and give up after
 // MHD_NCCL_TIMEOUT_S seconds (default 600): the communicator is aborted and the context gets
 // the sticky MHD_E_NCCL (a rank that died or stopped calling would otherwise hang every
 // synchronising call; SPEC.md:106's neighbour timeout).
 int sync_stream(mhd_ctx* c) {
-  if (!(c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL && c->comm)) {
+  if (!nccl_active(c)) {
     CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
     return MHD_OK;
   }
@@ -245,7 +256,7 @@ int fill_z_ghosts_local(mhd_ctx* c, double* U) {
   const int nz = c->nzl, g = c->gz;
   auto P = [&](int zs) { return U + (size_t)zs * pe; };
   const bool peri = c->bc_lo[2] == MHD_BC_PERIODIC;
-  if (c->nranks == 1 && peri) {  // U[-m] = U[N-m], U[N-1+m] = U[m-1]: two contiguous g-plane blocks
+  if (c->nranks == 1 && peri && !c->nccl_self) {  // U[-m] = U[N-m], U[N-1+m] = U[m-1]: two contiguous g-plane blocks
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(0), P(nz), g * pb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_OR_RETURN(c, cudaMemcpyAsync(P(nz + g), P(g), g * pb, cudaMemcpyDeviceToDevice, c->stream));
   }
@@ -263,8 +274,13 @@ int fill_z_ghosts_local(mhd_ctx* c, double* U) {
 int exchange_nccl(mhd_ctx* c, double* U) {
   const size_t pe = plane_elems(c);
   int plan[4][4];
-  if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, c->gz, plan))
+  if (c->nccl_self) {  // the periodic wrap as the two-rank plan with both neighbours = this rank
+    const int nz = c->nzl, g = c->gz;
+    const int rows[4][4] = {{0, 0, nz, g}, {0, 1, 0, g}, {0, 0, g, g}, {0, 1, nz + g, g}};
+    memcpy(plan, rows, sizeof plan);
+  } else if (halo_plan(c->rank, c->nranks, c->n[2], c->bc_lo[2] == MHD_BC_PERIODIC, c->gz, plan)) {
     return set_err(c, MHD_E_ARG, "halo plan");
+  }
   CUDA_OR_RETURN(c, cudaEventRecord(c->ev_ready, c->stream));
   CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
   NCCL_OR_RETURN(c, ncclGroupStart());
@@ -352,7 +368,7 @@ void prof_drain(mhd_ctx* c) {
 int whole_fill_ghosts(mhd_ctx* c, int stage) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
-  if (c->nranks > 1) {
+  if (slabbed(c)) {
     if ((rc = exchange(c, stage))) return rc;
     CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
   }
@@ -401,7 +417,7 @@ int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
   nvtxRangePushA(stage == 1 ? "mhd stage 1" : stage == 2 ? "mhd stage 2" : "mhd stage 3");
-  if (c->nranks > 1 && c->dim == 3) {
+  if (slabbed(c) && c->dim == 3) {
     nvtxRangePushA("mhd halo exchange");
     rc = exchange(c, stage);
     nvtxRangePop();
@@ -532,7 +548,7 @@ int reduce_and_read_(mhd_ctx* c) {
   prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "dt launch: %s", cudaGetErrorString(e));
   unsigned long long* src = c->dbuf;
-  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
+  if (nccl_active(c)) {
     // maxima (exact on the int64 patterns of non-negative doubles), counter sums, bad-slot minima
     NCCL_OR_RETURN(c, ncclGroupStart());
     NCCL_OR_RETURN(c, ncclAllReduce(c->dbuf, c->dred, 2, ncclUint64, ncclMax, c->comm, c->stream));
@@ -791,7 +807,9 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     return MHD_E_CUDA;
   }
   c->transport = dist ? dist->transport : MHD_TRANSPORT_NCCL;
-  if (c->nranks > 1) {  // the halo's stream and events (NCCL ranks and in-process slabs alike)
+  if (const char* e = getenv("MHD_NCCL_SELF"))
+    c->nccl_self = atoi(e) == 1 && c->nranks == 1 && c->dim == 3 && c->bc_lo[2] == MHD_BC_PERIODIC;
+  if (c->nranks > 1 || c->nccl_self) {  // the halo's stream and events (NCCL ranks and in-process slabs alike)
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
@@ -799,9 +817,16 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
       return MHD_E_CUDA;
     }
   }
-  if (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) {
+  if ((c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) || c->nccl_self) {
     ncclUniqueId id;
-    memcpy(&id, dist->nccl_id, sizeof id);
+    if (c->nccl_self) {
+      if (ncclGetUniqueId(&id) != ncclSuccess) {
+        mhd_destroy(c);
+        return MHD_E_NCCL;
+      }
+    } else {
+      memcpy(&id, dist->nccl_id, sizeof id);
+    }
     if (ncclCommInitRank(&c->comm, c->nranks, id, c->rank) != ncclSuccess) {
       c->comm = nullptr;
       mhd_destroy(c);

@@ -1024,3 +1024,40 @@ def test_profile_exposed_halo_class_on_slabs(mhd):
     s.run(2)
     assert s.profile_read_stages()["halo_exposed"] == (0.0, 0)
     s.destroy()
+
+
+@pytest.mark.parametrize("scheme", ["plm-rk2", "wenoz-rk3", "ct-rk2"])
+def test_nccl_self_exchange_bitwise(mhd, scheme):
+    """The NCCL code path of the multi-GPU run on one GPU (MHD_NCCL_SELF=1): a one-rank NCCL
+    communicator exchanges the periodic z ghost planes by ncclSend/ncclRecv to itself through the
+    ranks' stage schedule (interior launch while the halo runs on the comm stream, boundary
+    launches after the halo event; CT and split WENO-Z wait for it) and reduces dt, counters and
+    bad cells with ncclAllReduce — bitwise equal to the device-copy path with equal counters."""
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
+    if scheme == "wenoz-rk3":
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    if scheme == "ct-rk2":
+        p = I.ct_problem(I.orszag_tang_3d(16))
+    U0 = I.orszag_tang_3d_ic(p.replace(ct=0, glm=1) if p.ct else p)
+    U0 = np.ascontiguousarray(U0[:8] if p.ct else I.with_noise(U0, p))
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(4)
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    os.environ["MHD_NCCL_SELF"] = "1"
+    try:
+        s = mhd.Solver(p)
+    finally:
+        os.environ.pop("MHD_NCCL_SELF", None)
+    s.set_state(U0)
+    s.profile_enable(True, capacity=64)
+    logN = s.run(4)
+    prof = s.profile_read_stages()
+    UN, dN = s.get_state(), s.diag()
+    s.destroy()
+    assert np.array_equal(log1, logN) and np.array_equal(U1, UN)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dN[k]
+    if scheme == "plm-rk2":  # the fused stage ran the split schedule (one exposed-halo pair per stage)
+        assert prof["halo_exposed"][1] == 8
