@@ -485,16 +485,16 @@ def main():
     e2e = None
     e2e_note = "--no-e2e" if args.no_e2e else None
     if not args.no_e2e and small:
-        # two pinned host copies of this rank's state per rank on the node: leave half the host RAM
+        # two pinned host copies of the state per rank on the node must fit in 80% of the free host RAM
         try:
             import psutil
             avail = psutil.virtual_memory().available
         except Exception:
             avail = None
         need = 2 * U0.nbytes * int(os.environ.get("LOCAL_WORLD_SIZE", world))
-        if avail is not None and need > avail // 2:
+        if avail is not None and need > 0.8 * avail:
             small = False
-            e2e_note = f"not measured: {need / 1e9:.0f} GB of pinned host buffers exceed half the free host RAM"
+            e2e_note = f"not measured: {need / 1e9:.0f} GB of pinned host buffers exceed 80% of the free host RAM"
     if not args.no_e2e and small:
         Uh = torch.from_numpy(U0).pin_memory()
         Uo = torch.empty_like(Uh).pin_memory()
