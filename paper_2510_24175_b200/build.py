@@ -50,6 +50,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
            "-shared", "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines],
+           *os.environ.get("MHD_NVCC_EXTRA", "").split(),  # (A/B builds only)
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", OUT + ".tmp"]
     if verbose:
