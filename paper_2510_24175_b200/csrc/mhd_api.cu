@@ -413,10 +413,9 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
 // planes [g, nz-g) run (their stencil reads no ghost plane), then — after `ev_halo` — the g + g
 // boundary planes.  One slab: the ghost copies and one whole launch.  One profiling pair spans
 // the stage.
-int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+int fused_stage_body(mhd_ctx* c, int stage, const StageConsts& k) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
-  nvtxRangePushA(stage == 1 ? "mhd stage 1" : stage == 2 ? "mhd stage 2" : "mhd stage 3");
   if (slabbed(c) && c->dim == 3) {
     nvtxRangePushA("mhd halo exchange");
     rc = exchange(c, stage);
@@ -434,12 +433,16 @@ int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
     if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
     if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
     prof_end(c, pr);
-    nvtxRangePop();
     return MHD_OK;
   }
   const int pr = prof_begin(c, stage);
   rc = run_stage(c, stage, k, 0, c->nzl);
   prof_end(c, pr);
+  return rc;
+}
+int fused_stage(mhd_ctx* c, int stage, const StageConsts& k) {
+  nvtxRangePushA(stage == 1 ? "mhd stage 1" : stage == 2 ? "mhd stage 2" : "mhd stage 3");
+  const int rc = fused_stage_body(c, stage, k);
   nvtxRangePop();
   return rc;
 }
