@@ -8,7 +8,9 @@ boundary launches and how much of the halo ran under the interior launch.
   MHD_NCCL_SELF=1 python tools/timeline.py --out profiles/r02_timeline_nccl_self.json
       one periodic rank, the z halo through NCCL (send/recv to itself) on the comm stream
   python tools/timeline.py --slabs 4 --out ...   in-process slabs (device-copy halo)
-Under torchrun (NCCL ranks) the same script traces each rank (--out gets a rank suffix).
+  python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 tools/timeline.py --n 1024 \
+      --out timeline.json      NCCL ranks: the global n^3 box in z slabs, one trace per rank
+      (timeline.rank<r>.json) with the NCCL send/recv kernels beside the interior launches
 """
 import argparse
 import json
@@ -44,11 +46,26 @@ def main():
     from paper_2510_24175_b200 import inputs as I
     from paper_2510_24175_b200 import mhd
     p = I.orszag_tang_3d(args.n)
-    U0 = I.workload_ic("ot3d", p, 0, p.n[2])
-    if args.slabs > 1:
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    if world > 1:  # NCCL ranks (torchrun): the global n^3 box split into z slabs, one trace per rank
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [mhd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        solver = mhd.Solver(p, rank=rank, nranks=world, device=local, nccl_id=obj[0],
+                            stream=torch.cuda.current_stream())
+        z0, nz = solver.offset[2], solver.extent[2]
+        U0 = I.workload_ic("ot3d", p, z0, z0 + nz)
+        root, ext = os.path.splitext(args.out)
+        args.out = f"{root}.rank{rank}{ext}"
+    elif args.slabs > 1:
+        U0 = I.workload_ic("ot3d", p, 0, p.n[2])
         solver = mhd.SolverGroup(p, args.slabs)
         solver.slabs[0].set_stream(torch.cuda.current_stream())
     else:
+        U0 = I.workload_ic("ot3d", p, 0, p.n[2])
         solver = mhd.Solver(p, stream=torch.cuda.current_stream())
     solver.set_state(U0)
     solver.run(2)
@@ -62,7 +79,8 @@ def main():
     iv = intervals(trace)
     stages = [e for e in iv if "k_stage" in e["name"]]
     halo = [e for e in iv if "nccl" in e["name"].lower() or e["cat"] == "gpu_memcpy"]
-    summary = {"n": args.n, "slabs": args.slabs, "steps": args.steps, "nccl_self": os.environ.get("MHD_NCCL_SELF") == "1",
+    summary = {"n": args.n, "slabs": args.slabs, "ranks": world, "rank": rank, "steps": args.steps,
+               "nccl_self": os.environ.get("MHD_NCCL_SELF") == "1",
                "stage_launches": len(stages), "halo_events": len(halo),
                "kernels": sorted({e["name"][:60] for e in iv}), "stages": []}
     # per stage: the long (interior) launch and the halo events that ran beside it
@@ -76,6 +94,9 @@ def main():
                                   "halo_under_interior_frac": ov / tot if tot > 0 else None,
                                   "halo": [(e["name"][:40], round(e["end"] - e["ts"], 1), e["stream"]) for e in h]})
     print(json.dumps(summary), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
