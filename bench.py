@@ -8,8 +8,8 @@ and ncclAllReduce(max) for dt inside the library):
                    single-GPU 512^3 run of the same fused kernel.
   --scaling strong BASELINE configs[4]: 3D Orszag-Tang 1024^3 (the north star's scaling target),
                    split into N z slabs of 1024/N planes.
---workload / --n override the problem (e.g. --workload ot3d --n 256: configs[2], the 256^3
-single-GPU roofline run; with --scaling weak --n is per GPU, with strong it is global).
+--workload / --size (alias --n) override the problem (e.g. --workload ot3d --size 256: configs[2], the
+256^3 single-GPU roofline run; with --scaling weak the size is per GPU, with strong it is global).
 Scheme (both modes): PLM-MC + HLLD + GLM, SSP-RK2, CFL 0.4 (--scheme for the paper's others).
 
 A step is one user-loop iteration: dt = mhd_compute_dt() (k_dt + a 72-byte read-back) then
@@ -345,7 +345,9 @@ def main():
     ap.add_argument("--impl", default="mhd", choices=["mhd", "reference"])
     ap.add_argument("--scaling", default="weak", choices=sorted(SCALING),
                     help="weak: configs[3] blast 512^3 per GPU (default); strong: configs[4] OT 1024^3 split over N")
-    ap.add_argument("--n", type=int, default=None, help="cells per axis (weak: per GPU; strong: global)")
+    ap.add_argument("--size", "--n", dest="n", type=int, default=None,
+                    help="cells per axis (weak: per GPU; strong: global); under torchrun use --size "
+                         "(torchrun's own parser takes --n for --nnodes)")
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--scheme", default="plm-rk2", choices=sorted(SCHEMES),
                     help="plm-rk2: the north star's PLM-MC + HLLD + GLM + SSP-RK2 (default); wenoz-rk3: the "

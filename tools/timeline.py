@@ -8,7 +8,7 @@ boundary launches and how much of the halo ran under the interior launch.
   MHD_NCCL_SELF=1 python tools/timeline.py --out profiles/r02_timeline_nccl_self.json
       one periodic rank, the z halo through NCCL (send/recv to itself) on the comm stream
   python tools/timeline.py --slabs 4 --out ...   in-process slabs (device-copy halo)
-  python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 tools/timeline.py --n 1024 \
+  python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 tools/timeline.py --size 1024 \
       --out timeline.json      NCCL ranks: the global n^3 box in z slabs, one trace per rank
       (timeline.rank<r>.json) with the NCCL send/recv kernels beside the interior launches
 """
@@ -36,7 +36,7 @@ def overlap(a, b):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=256)  # (--n is torchrun's under torchrun)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--slabs", type=int, default=1)
     ap.add_argument("--out", default="gpurun_out/timeline.json")
