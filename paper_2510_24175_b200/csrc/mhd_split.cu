@@ -111,7 +111,7 @@ __device__ __forceinline__ bool sp_recon(const SplitArgs& a, const SpIdx& X, int
     for (int f = 0; f < NVS; ++f) c[s + 2][f] = v[f * fs];
   }
 #ifndef MHD_SP_INL
-#define MHD_SP_INL 1  // bit D: inline WENO-Z in the D-face kernel (x only: -2%; y, z slower inlined)
+#define MHD_SP_INL 0  // bit D: inline WENO-Z in the D-face kernel (round 2: all out of line, 8.40 vs 8.45 ms with x inline)
 #endif
   const bool fb = weno_cell<NVS, (MHD_SP_INL >> D) & 1>(c[0], c[1], c[2], c[3], c[4], p, m);
   to_normal<NVS, D>(p, qp);
