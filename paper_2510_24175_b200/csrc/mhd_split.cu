@@ -135,7 +135,7 @@ __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* 
 }
 
 #ifndef MHD_SP_SEG
-#define MHD_SP_SEG 32
+#define MHD_SP_SEG 64
 #endif
 constexpr int kSpSeg = MHD_SP_SEG;  // faces per marching segment (at most; segments of a line are balanced)
 #ifndef MHD_SP_MINB
