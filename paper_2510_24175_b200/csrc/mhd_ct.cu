@@ -21,6 +21,10 @@
 #include "mhd_device.cuh"
 #include "mhd_kernels.h"
 
+#ifndef MHD_CT_WINL
+#define MHD_CT_WINL true  // WENO-Z evaluator inlined in the CT face kernels
+#endif
+
 namespace mhd {
 
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
@@ -95,7 +99,7 @@ __device__ __forceinline__ bool ct_recon(const CtArgs& a, const CtIdx& X, int i,
   for (int s = -H; s <= H; ++s)
 #pragma unroll
     for (int f = 0; f < 8; ++f) c[s + H][f] = a.V[X.at(f, i + s * oi, j + s * oj, k + s * ok)];
-  if constexpr (REC == 2) return weno_cell<8, true>(c[0], c[1], c[2], c[3], c[4], qp, qm);
+  if constexpr (REC == 2) return weno_cell<8, MHD_CT_WINL>(c[0], c[1], c[2], c[3], c[4], qp, qm);
   else return plm_cell<8, REC>(c[0], c[1], c[2], qp, qm);
 }
 
@@ -118,7 +122,10 @@ __device__ __forceinline__ int ct_solve_store(const CtArgs& a, const CtIdx& X, d
   return fell;
 }
 
-constexpr int kCtSeg = 16;  // cells per marching segment (one extra reconstruction per segment)
+#ifndef MHD_CT_SEG
+#define MHD_CT_SEG 32
+#endif
+constexpr int kCtSeg = MHD_CT_SEG;  // cells per marching segment (one extra reconstruction per segment)
 #ifndef MHD_CT_MINB
 #define MHD_CT_MINB 4  // 4 blocks of 128 per SM (<= 128 registers): -7% CT-WENOZ stage time, -3% CT-PLM
 #endif
