@@ -127,12 +127,19 @@ __device__ __forceinline__ int ct_solve_store(const CtArgs& a, const CtIdx& X, d
 #endif
 constexpr int kCtSeg = MHD_CT_SEG;  // cells per marching segment (one extra reconstruction per segment)
 #ifndef MHD_CT_MINB
-#define MHD_CT_MINB 4  // 4 blocks of 128 per SM (<= 128 registers): -7% CT-WENOZ stage time, -3% CT-PLM
+#define MHD_CT_MINB 4  // PLM: 4 blocks of 128 per SM (<= 128 registers): -3% CT-PLM stage time
 #endif
+#ifndef MHD_CT_MINB_W
+#define MHD_CT_MINB_W 3  // WENO-Z: 3 blocks (<= 168 registers, fewer spills): 6.8-6.9 vs 7.05 ms (4 blocks)
+#endif
+template <int REC>
+struct CtMinB {
+  static constexpr int value = REC == 2 ? MHD_CT_MINB_W : MHD_CT_MINB;
+};
 
 // y (D = 1) and z (D = 2) faces: a thread marches a segment of one line (lane = x, coalesced)
 template <int D, int RS, int REC>
-__global__ void __launch_bounds__(128, MHD_CT_MINB) k_ct_face_m(CtArgs a) {
+__global__ void __launch_bounds__(128, CtMinB<REC>::value) k_ct_face_m(CtArgs a) {
   const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
   const int nb = D == 1 ? a.nz + 2 : a.ny;     // second line coordinate: k + 1 (y) or j (z)
   const int nm = D == 1 ? a.ny : a.nz + 1;     // marched faces per line
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(128, MHD_CT_MINB) k_ct_face_m(CtArgs a) {
 // x faces: warps over 32-cell chunks of the rows (j, k), k in [-1, nz]; lane l > 0 takes q+ of
 // cell i-1 from lane l-1; the faces at chunk starts follow in a second pass, one per thread
 template <int RS, int REC>
-__global__ void __launch_bounds__(128, MHD_CT_MINB) k_ct_face_x(CtArgs a) {
+__global__ void __launch_bounds__(128, CtMinB<REC>::value) k_ct_face_x(CtArgs a) {
   const CtIdx X{a.nx, a.ny, a.nz, a.gz, (size_t)a.nx * a.ny, (size_t)a.nx * a.ny * 8};
   const int nch = (a.nx + 31) / 32;
   const size_t items = (size_t)nch * a.ny * (a.nz + 2);
