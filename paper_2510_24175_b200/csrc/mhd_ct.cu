@@ -122,6 +122,9 @@ __device__ __forceinline__ int ct_solve_store(const CtArgs& a, const CtIdx& X, d
   return fell;
 }
 
+#ifndef MHD_CTU_PER_SM
+#define MHD_CTU_PER_SM 64  // k_ct_prim / k_ct_update blocks of 256 per SM
+#endif
 #ifndef MHD_CT_SEG
 #define MHD_CT_SEG 32
 #endif
@@ -275,7 +278,7 @@ static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st, cudaSt
   auto grid = [&](size_t n, int bs, int per_sm) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((n + bs - 1) / bs, (size_t)nsm * per_sm));
   };
-  k_ct_prim<<<grid(pc * (a.nz + 2 * a.G), 256, 16), 256, 0, st>>>(a);
+  k_ct_prim<<<grid(pc * (a.nz + 2 * a.G), 256, MHD_CTU_PER_SM), 256, 0, st>>>(a);
   // the three face kernels are independent: y and z on two auxiliary streams, joined before
   // the update
   cudaStream_t s1 = aux1 ? aux1 : st, s2 = aux2 ? aux2 : st;
@@ -295,7 +298,7 @@ static cudaError_t launch_ct_t(const CtArgs& a, int nsm, cudaStream_t st, cudaSt
     cudaStreamWaitEvent(st, ev[1], 0);
     cudaStreamWaitEvent(st, ev[2], 0);
   }
-  k_ct_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
+  k_ct_update<<<grid(pc * a.nz, 256, MHD_CTU_PER_SM), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

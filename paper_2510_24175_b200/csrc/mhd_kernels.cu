@@ -213,6 +213,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
 
 // ---------------------------------------------------------------------------------------
 // fused stage kernel
+#ifndef MHD_DT_PER_SM
+#define MHD_DT_PER_SM 32 // k_dt blocks of 256 per SM in the grid (each loops over its planes)
+#endif
 #ifndef MHD_ZTMA
 #define MHD_ZTMA 1
 #endif
@@ -1037,7 +1040,7 @@ int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter) {
 
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st) {
   // ~8 blocks of 256 per SM in total: x covers a plane (capped), y strides over the planes
-  const size_t fs = (size_t)a.nx * a.ny, cap = (size_t)nsm * 8;
+  const size_t fs = (size_t)a.nx * a.ny, cap = (size_t)nsm * MHD_DT_PER_SM;
   const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>((fs + 255) / 256, cap));
   const unsigned by = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)a.nz_loc, cap / bx));
   const dim3 g(bx, by);

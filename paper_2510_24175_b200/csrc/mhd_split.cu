@@ -137,7 +137,16 @@ __device__ __forceinline__ int sp_solve_store(const SplitArgs& a, const double* 
 #ifndef MHD_SP_SEG
 #define MHD_SP_SEG 64
 #endif
-constexpr int kSpSeg = MHD_SP_SEG;  // faces per marching segment (at most; segments of a line are balanced)
+constexpr int kSpSeg = MHD_SP_SEG;
+#ifndef MHD_SPP_PER_SM
+#define MHD_SPP_PER_SM 64  // k_sp_prim blocks of 256 per SM
+#endif
+#ifndef MHD_SPF_PER_SM
+#define MHD_SPF_PER_SM 32  // face-kernel blocks of 128 per SM
+#endif
+#ifndef MHD_SPU_PER_SM
+#define MHD_SPU_PER_SM 256 // k_sp_update blocks of 256 per SM (grid-stride over the cells)
+#endif  // faces per marching segment (at most; segments of a line are balanced)
 #ifndef MHD_SP_MINB
 #define MHD_SP_MINB 3  // 3 blocks of 128 per SM (<= 168 registers): +2% over no bound, 4 spills more
 #endif
@@ -247,7 +256,7 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
   const size_t segy = (size_t)a.nx * a.nz * ((a.ny + 1 + kSpSeg - 1) / kSpSeg);
   const size_t segz = (size_t)a.nx * a.ny * ((a.nz + 1 + kSpSeg - 1) / kSpSeg);
   const size_t xw = (size_t)((a.nx + 1 + 30) / 31) * 32 * a.ny * a.nz;
-  k_sp_prim<<<grid(pc * (a.nz + 6), 256, 16), 256, 0, st>>>(a);
+  k_sp_prim<<<grid(pc * (a.nz + 6), 256, MHD_SPP_PER_SM), 256, 0, st>>>(a);
   // the three face kernels are independent (V in, their own F out): y and z on two auxiliary
   // streams, joined before the update, so one kernel's tail overlaps the others
   cudaStream_t s1 = aux1 ? aux1 : st, s2 = aux2 ? aux2 : st;
@@ -257,13 +266,13 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
     cudaStreamWaitEvent(s2, ev[0], 0);
   }
   if (riemann) {
-    k_sp_face_x<1><<<grid(xw, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<1, 1><<<grid(segy, 128, 32), 128, 0, s1>>>(a);
-    k_sp_face_m<2, 1><<<grid(segz, 128, 32), 128, 0, s2>>>(a);
+    k_sp_face_x<1><<<grid(xw, 128, MHD_SPF_PER_SM), 128, 0, st>>>(a);
+    k_sp_face_m<1, 1><<<grid(segy, 128, MHD_SPF_PER_SM), 128, 0, s1>>>(a);
+    k_sp_face_m<2, 1><<<grid(segz, 128, MHD_SPF_PER_SM), 128, 0, s2>>>(a);
   } else {
-    k_sp_face_x<0><<<grid(xw, 128, 32), 128, 0, st>>>(a);
-    k_sp_face_m<1, 0><<<grid(segy, 128, 32), 128, 0, s1>>>(a);
-    k_sp_face_m<2, 0><<<grid(segz, 128, 32), 128, 0, s2>>>(a);
+    k_sp_face_x<0><<<grid(xw, 128, MHD_SPF_PER_SM), 128, 0, st>>>(a);
+    k_sp_face_m<1, 0><<<grid(segy, 128, MHD_SPF_PER_SM), 128, 0, s1>>>(a);
+    k_sp_face_m<2, 0><<<grid(segz, 128, MHD_SPF_PER_SM), 128, 0, s2>>>(a);
   }
   if (aux1) {
     cudaEventRecord(ev[1], s1);
@@ -271,7 +280,7 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
     cudaStreamWaitEvent(st, ev[1], 0);
     cudaStreamWaitEvent(st, ev[2], 0);
   }
-  k_sp_update<<<grid(pc * a.nz, 256, 16), 256, 0, st>>>(a);
+  k_sp_update<<<grid(pc * a.nz, 256, MHD_SPU_PER_SM), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
