@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256) k_ct_dt(DtArgs a) {
 
 cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st) {
   const size_t n = (size_t)a.nx * a.ny * a.nz_loc;
-  const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 8);
+  const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)nsm * 32);
   k_ct_dt<<<g > 0 ? g : 1, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
