@@ -147,13 +147,17 @@ constexpr int kSpSeg = MHD_SP_SEG;
 #ifndef MHD_SPU_PER_SM
 #define MHD_SPU_PER_SM 256 // k_sp_update blocks of 256 per SM (grid-stride over the cells)
 #endif  // faces per marching segment (at most; segments of a line are balanced)
+#ifndef MHD_SP_BLOCK
+#define MHD_SP_BLOCK 128  // face-kernel block size
+#endif
+constexpr int kSpB = MHD_SP_BLOCK;
 #ifndef MHD_SP_MINB
 #define MHD_SP_MINB 3  // 3 blocks of 128 per SM (<= 168 registers): +2% over no bound, 4 spills more
 #endif
 
 // y and z faces: lane = x (coalesced), a thread marches one 16-face segment of a line
 template <int D, int RS>
-__global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_m(SplitArgs a) {
+__global__ void __launch_bounds__(kSpB, MHD_SP_MINB) k_sp_face_m(SplitArgs a) {
   const SpIdx X = make_idx(a);
   const int nb = D == 1 ? a.nz : a.ny;         // second line coordinate: k (y lines) or j (z lines)
   const int nm = D == 1 ? a.ny + 1 : a.nz + 1;  // faces per line
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_m(SplitArgs a) {
 // second pass (the lane-0 cell is reconstructed twice: 1/32 of the work) and every read is a
 // coalesced row segment that the neighbouring items also touch (L1/L2 hits, V read once from HBM).
 template <int RS>
-__global__ void __launch_bounds__(128, MHD_SP_MINB) k_sp_face_x(SplitArgs a) {
+__global__ void __launch_bounds__(kSpB, MHD_SP_MINB) k_sp_face_x(SplitArgs a) {
   const SpIdx X = make_idx(a);
   const int nf = a.nx + 1, nch = (nf + 30) / 31;  // faces per row, items per row
   const size_t items = (size_t)nch * a.ny * a.nz;
@@ -266,13 +270,13 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
     cudaStreamWaitEvent(s2, ev[0], 0);
   }
   if (riemann) {
-    k_sp_face_x<1><<<grid(xw, 128, MHD_SPF_PER_SM), 128, 0, st>>>(a);
-    k_sp_face_m<1, 1><<<grid(segy, 128, MHD_SPF_PER_SM), 128, 0, s1>>>(a);
-    k_sp_face_m<2, 1><<<grid(segz, 128, MHD_SPF_PER_SM), 128, 0, s2>>>(a);
+    k_sp_face_x<1><<<grid(xw, kSpB, MHD_SPF_PER_SM), kSpB, 0, st>>>(a);
+    k_sp_face_m<1, 1><<<grid(segy, kSpB, MHD_SPF_PER_SM), kSpB, 0, s1>>>(a);
+    k_sp_face_m<2, 1><<<grid(segz, kSpB, MHD_SPF_PER_SM), kSpB, 0, s2>>>(a);
   } else {
-    k_sp_face_x<0><<<grid(xw, 128, MHD_SPF_PER_SM), 128, 0, st>>>(a);
-    k_sp_face_m<1, 0><<<grid(segy, 128, MHD_SPF_PER_SM), 128, 0, s1>>>(a);
-    k_sp_face_m<2, 0><<<grid(segz, 128, MHD_SPF_PER_SM), 128, 0, s2>>>(a);
+    k_sp_face_x<0><<<grid(xw, kSpB, MHD_SPF_PER_SM), kSpB, 0, st>>>(a);
+    k_sp_face_m<1, 0><<<grid(segy, kSpB, MHD_SPF_PER_SM), kSpB, 0, s1>>>(a);
+    k_sp_face_m<2, 0><<<grid(segz, kSpB, MHD_SPF_PER_SM), kSpB, 0, s2>>>(a);
   }
   if (aux1) {
     cudaEventRecord(ev[1], s1);
