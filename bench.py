@@ -84,6 +84,15 @@ class ClockSampler:
         self.nv = None
         self.stop = threading.Event()
 
+    def _nvml_handle(self, nv):
+        """the NVML handle of CUDA device `index` (by UUID: CUDA_VISIBLE_DEVICES may renumber)"""
+        try:
+            import torch
+            u = str(torch.cuda.get_device_properties(self.index).uuid)
+            return nv.nvmlDeviceGetHandleByUUID(u if u.startswith("GPU-") else "GPU-" + u)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
     def _nvml_sample(self):
         nv, h = self.nv, self.h
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -106,7 +115,7 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv, self.h = pynvml, self._nvml_handle(pynvml)
             self._nvml_sample()
             self.t = threading.Thread(target=self._nvml_loop, daemon=True)
             self.t.start()
