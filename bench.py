@@ -362,9 +362,15 @@ def main():
                     help="plm-rk2: the north star's PLM-MC + HLLD + GLM + SSP-RK2 (default); wenoz-rk3: the "
                          "paper's strong-scaling WENOZ + HLLD + GLM + SSP-RK3 (PAPER.md:270); ct-wenoz-rk3: its "
                          "weak-scaling WENOZ + HLLD + CT + SSP-RK3 (PAPER.md:179)")
+    ap.add_argument("--halo", default="exchange", choices=["exchange", "push"],
+                    help="z slabs: exchange = NCCL send/recv overlapped with the interior launch (default); "
+                         "push = each stage's epilogue stores its boundary planes into the neighbours' NCCL "
+                         "symmetric windows, one launch + an LSA barrier per stage (MHD_HALO_PUSH, DESIGN.md §8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.halo == "push":
+        os.environ["MHD_HALO_PUSH"] = "1"
     args.warmup = max(args.warmup, 3) if args.impl == "mhd" else args.warmup
     # the oracle's OpenMP threads stay on their cores (read when libgomp initialises)
     os.environ.setdefault("OMP_PROC_BIND", "close")
@@ -396,6 +402,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     s = mhd.Solver(p, rank=rank, nranks=world, device=local_rank, nccl_id=nccl_id)
+    push = s.halo_push  # (set up, and agreed over the ranks, by mhd_create)
     assert s.offset[2] == z0 and s.extent[2] == z1 - z0
     stream = torch.cuda.current_stream()
     s.set_stream(stream)
@@ -543,7 +550,8 @@ def main():
     # launches with slabs: interior and the two boundary ranges), or five launches for CT and for
     # the 3D GLM WENO-Z split stage (mhd_split.cu; MHD_FUSED_WENOZ=1 selects the fused kernel)
     split = (p.limiter == I.WENOZ and p.n[2] > 1 and not p.ct and os.environ.get("MHD_FUSED_WENOZ") != "1")
-    launches_per_stage = 5 if (p.ct or split) else (3 if world > 1 else 1)
+    # (halo push: the stage launch and the LSA barrier kernel)
+    launches_per_stage = 5 if (p.ct or split) else (2 if push else 3 if world > 1 else 1)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -551,6 +559,8 @@ def main():
                 "config": {"workload": label, "problem": WORKLOADS[wl], "global": list(p.n),
                            "per_gpu": [p.n[0], p.n[1], p.n[2] // world], "scheme": SCHEMES[args.scheme],
                            "cells": cells, "parallelism": f"z-slab x{world}",
+                           "halo": ("push (stage epilogue -> NCCL symmetric windows)" if push else
+                                    "exchange (NCCL send/recv beside the interior launch)") if world > 1 else None,
                            "l2": f"inputs larger than L2 (2 x {U0.nbytes / 1e9:.2f} GB state arrays per GPU)"},
                 "roofline": roof, "clocks": clk.summary(),
                 "gpu_launches": args.steps * (2 + nst * launches_per_stage),

@@ -249,6 +249,21 @@ int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
  * slab).  The stage intervals include their halo wait. */
 int mhd_profile_read_stages(mhd_ctx* ctx, double ms[5], int64_t units[5]);
 
+/* Halo push (the z halo of each RK stage).  With the
+ * environment variable MHD_HALO_PUSH=1 at mhd_create, a 3D slab context of the fused stage
+ * (PLM or fused WENO-Z, GLM; not CT, not the split WENO-Z stage) has each stage's epilogue store
+ * its g boundary planes also into the z neighbours' ghost planes of the next stage's input, so
+ * the next stage runs as one launch with no exchange.  NCCL ranks: the state arrays are NCCL
+ * symmetric windows (ncclMemAlloc, ncclCommWindowRegister; every neighbour must be reachable
+ * by load/store, i.e. on the same node), and a one-CTA NCCL LSA barrier after every pushing
+ * stage orders the ranks; the set-up is agreed over all ranks, and if any step of it fails on
+ * any rank no rank pushes (the send/recv exchange stays in use).  In-process slab groups: the
+ * neighbour slabs' arrays.  The first stage after a state change (mhd_set_state*,
+ * mhd_bind_workspace) exchanges as before.  Results are bitwise those of the exchange.
+ * Returns 1 if the context pushes, 0 if not, MHD_E_ARG for a null context.  With pushing NCCL
+ * ranks mhd_bind_workspace fails with MHD_E_STATE (the arrays are windows). */
+int mhd_halo_push(const mhd_ctx* ctx);
+
 /* Library build identity, e.g. "libmhd sm_100a fused-v1". */
 const char* mhd_version(void);
 

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmhd.so")
-SOURCES = ["mhd_kernels.cu", "mhd_ct.cu", "mhd_split.cu", "mhd_api.cu"]
+SOURCES = ["mhd_kernels.cu", "mhd_ct.cu", "mhd_split.cu", "mhd_push.cu", "mhd_api.cu"]
 DEPS = SOURCES + ["mhd_device.cuh", "mhd_kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         return OUT
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "--threads", "0", "-Xcompiler", "-fPIC,-O2",
            "-shared", "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines],
            *os.environ.get("MHD_NVCC_EXTRA", "").split(),  # (A/B builds only)
            *[os.path.join(CSRC, s) for s in SOURCES],

@@ -71,6 +71,21 @@ struct mhd_ctx {
   cudaStream_t comm_stream = nullptr;            // NCCL halo exchange (overlaps the interior)
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   mhd_ctx* const* group = nullptr;                // MHD_TRANSPORT_LOCAL: the slabs of this group
+  // halo push (MHD_HALO_PUSH=1; 3D fused stages on slabs): each stage's epilogue stores its g
+  // boundary planes into the z neighbours' ghost planes of the next stage's input, so the next
+  // stage needs no exchange and runs as one launch (§8).  NCCL ranks: the arrays are symmetric
+  // windows, the peers' arrays plain pointers into NVLink peer memory, and a one-CTA LSA
+  // barrier after each pushing stage orders the ranks; in-process slabs: the peer slabs'
+  // arrays, one stream.
+  bool push = false;                              // the transport is set up for pushing
+  bool push_valid = false;                        // the next stage's input ghost planes were pushed
+  double* peer_dn[3] = {nullptr, nullptr, nullptr};  // down / up neighbour's U0, U1, U2
+  double* peer_up[3] = {nullptr, nullptr, nullptr};
+  int peer_dn_nz = 0;
+  bool nccl_mem = false;                          // U0..U2 from ncclMemAlloc (windows)
+  size_t nccl_mem_bytes = 0;
+  ncclWindow_t win[3] = {nullptr, nullptr, nullptr};
+  std::vector<unsigned char> devcomm;             // ncclDevComm (one LSA barrier), opaque here
   int nsm = 148;
   int kz = 32;
   // cached step state
@@ -134,6 +149,13 @@ bool slabbed(const mhd_ctx* c) { return c->nranks > 1 || c->nccl_self; }
 // its halo and reductions go through an NCCL communicator
 bool nccl_active(const mhd_ctx* c) {
   return c->comm && ((c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) || c->nccl_self);
+}
+// the role (0 U^n, 1 U*/U1, 2 U2) of one of the context's state arrays
+int role_of(const mhd_ctx* c, const double* p) { return p == c->U0 ? 0 : p == c->U1 ? 1 : 2; }
+// MHD_HALO_PUSH=1 asks for the halo push; it applies to the fused 3D stages on slabs
+bool push_requested(const mhd_ctx* c) {
+  const char* e = getenv("MHD_HALO_PUSH");
+  return e && atoi(e) == 1 && c->dim == 3 && !c->scheme.ct && !c->split && (c->nranks > 1 || c->nccl_self);
 }
 
 // Host wait for the context's stream.  With NCCL slabs the stream may wait on collectives of
@@ -402,6 +424,14 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
+  a.push_dn = a.push_up = nullptr;
+  a.push_dn_nz = 0;
+  if (c->push) {  // this stage's boundary planes also go to the neighbours' ghost planes of sp.out
+    const int r = role_of(c, sp.out);
+    a.push_dn = c->peer_dn[r];
+    a.push_up = c->peer_up[r];
+    a.push_dn_nz = c->peer_dn_nz;
+  }
   cudaError_t e = mhd::launch_stage(c->dim, c->nv, c->scheme.riemann, a, c->stream);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "stage %d launch: %s", stage, cudaGetErrorString(e));
   return MHD_OK;
@@ -413,9 +443,27 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
 // planes [g, nz-g) run (their stencil reads no ghost plane), then — after `ev_halo` — the g + g
 // boundary planes.  One slab: the ghost copies and one whole launch.  One profiling pair spans
 // the stage.
+// after a pushing stage: NCCL ranks order the stage against every rank's next one
+int push_fence(mhd_ctx* c) {
+  if (nccl_active(c)) {
+    cudaError_t e = mhd::push_barrier(c->devcomm.data(), c->stream);
+    if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "push barrier: %s", cudaGetErrorString(e));
+  }
+  c->push_valid = true;
+  return MHD_OK;
+}
 int fused_stage_body(mhd_ctx* c, int stage, const StageConsts& k) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
+  if (slabbed(c) && c->dim == 3 && c->push && c->push_valid) {
+    // halo push: the input's ghost planes were stored by the neighbours' previous stage
+    // (ordered by the barrier after it): one launch over the whole slab
+    const int pr = prof_begin(c, stage);
+    if ((rc = run_stage(c, stage, k, 0, c->nzl))) return rc;
+    rc = push_fence(c);
+    prof_end(c, pr);
+    return rc;
+  }
   if (slabbed(c) && c->dim == 3) {
     nvtxRangePushA("mhd halo exchange");
     rc = exchange(c, stage);
@@ -432,6 +480,7 @@ int fused_stage_body(mhd_ctx* c, int stage, const StageConsts& k) {
     prof_end(c, pw);
     if ((rc = run_stage(c, stage, k, 0, lo))) return rc;
     if ((rc = run_stage(c, stage, k, hi, c->nzl))) return rc;
+    if (c->push && (rc = push_fence(c))) return rc;  // (the first stage after a state change)
     prof_end(c, pr);
     return MHD_OK;
   }
@@ -606,6 +655,7 @@ int io_setup(mhd_ctx* c) {
 int apply_input(mhd_ctx* c) {
   if (!c->in_pending) return MHD_OK;
   c->in_pending = false;
+  c->push_valid = false;
   c->sticky = MHD_OK;
   c->ch_valid = false;
   c->has_state = false;
@@ -621,6 +671,62 @@ int apply_input(mhd_ctx* c) {
                            c->stream, c->scheme.ct ? 0 : 1);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "validate: %s", cudaGetErrorString(e));
   c->has_state = true;
+  return MHD_OK;
+}
+
+// every rank's verdict: the minimum of `ok` over the communicator
+int agree(mhd_ctx* c, int ok) {
+  int* d = nullptr;
+  int h = ok;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 0;
+  bool fine = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+              ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, c->stream) == ncclSuccess &&
+              cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
+              cudaStreamSynchronize(c->stream) == cudaSuccess;
+  cudaFree(d);
+  return fine ? h : 0;
+}
+
+// NCCL halo push: register the state arrays as symmetric windows, create the device
+// communicator with one LSA barrier, and read the z neighbours' window addresses (NVLink peer
+// memory; the rank itself for MHD_NCCL_SELF).  Every step is agreed over the ranks, so either
+// all push or none does (then the send/recv exchange is used and the windows are released).
+int push_setup_nccl(mhd_ctx* c) {
+  int ok = agree(c, mhd::lsa_team_size(c->comm) == c->nranks);  // every neighbour load/store-accessible
+  double* arr[3] = {c->U0, c->U1, c->U2};
+  for (int r = 0; r < 3 && ok; ++r) {
+    if (!arr[r]) continue;
+    const int mine = ncclCommWindowRegister(c->comm, arr[r], c->nccl_mem_bytes, &c->win[r], NCCL_WIN_COLL_SYMMETRIC) ==
+                     ncclSuccess;
+    if (!mine) c->win[r] = nullptr;
+    ok = agree(c, mine);
+  }
+  if (ok) {
+    c->devcomm.assign(mhd::devcomm_bytes(), 0);
+    ok = agree(c, mhd::devcomm_create(c->comm, c->devcomm.data()) == 0);
+    if (!ok) c->devcomm.clear();
+  }
+  if (ok) {
+    double* p[6];
+    void* w[3] = {c->win[0], c->win[1], c->win[2]};
+    const int dn = c->nccl_self ? 0 : c->down, up = c->nccl_self ? 0 : c->up;
+    ok = agree(c, mhd::push_peer_pointers(w, dn, up, p, c->stream) == cudaSuccess);
+    for (int r = 0; r < 3 && ok; ++r) {
+      c->peer_dn[r] = p[2 * r];
+      c->peer_up[r] = p[2 * r + 1];
+    }
+    c->peer_dn_nz = c->nzl;  // (equal slabs)
+  }
+  if (!ok) {  // release what was set up; the exchange stays the send/recv path
+    cudaGetLastError();
+    if (!c->devcomm.empty()) mhd::devcomm_destroy(c->comm, c->devcomm.data());
+    c->devcomm.clear();
+    for (int r = 0; r < 3; ++r)
+      if (c->win[r]) ncclCommWindowDeregister(c->comm, c->win[r]);
+    for (int r = 0; r < 3; ++r) c->win[r] = nullptr, c->peer_dn[r] = c->peer_up[r] = nullptr;
+    return MHD_OK;
+  }
+  c->push = true;
   return MHD_OK;
 }
 
@@ -776,11 +882,25 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     c->kz = (int)(best_kz > 0 ? best_kz : 1);
   }
   c->arr_elems = plane_elems(c) * (size_t)(c->nzl + 2 * c->gz);
-  cudaError_t e1 = cudaMalloc(&c->U0, c->arr_elems * sizeof(double));
-  cudaError_t e2 = cudaMalloc(&c->U1, c->arr_elems * sizeof(double));
+  c->transport = dist ? dist->transport : MHD_TRANSPORT_NCCL;
+  if (const char* e = getenv("MHD_NCCL_SELF"))
+    c->nccl_self = atoi(e) == 1 && c->nranks == 1 && c->dim == 3 && c->bc_lo[2] == MHD_BC_PERIODIC;
+  const bool nccl_path = (c->nranks > 1 && c->transport == MHD_TRANSPORT_NCCL) || c->nccl_self;
+  const bool want_push = push_requested(c);
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  if (want_push && nccl_path) {  // the state arrays as NCCL symmetric windows (same size on every rank)
+    c->nccl_mem = true;
+    c->nccl_mem_bytes = (c->arr_elems * sizeof(double) + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+    double** arr[3] = {&c->U0, &c->U1, &c->U2};
+    for (int r = 0; r < (c->scheme.stepper == MHD_RK3 ? 3 : 2); ++r)
+      if (e1 == cudaSuccess && ncclMemAlloc((void**)arr[r], c->nccl_mem_bytes) != ncclSuccess) e1 = cudaErrorMemoryAllocation;
+  } else {
+    e1 = cudaMalloc(&c->U0, c->arr_elems * sizeof(double));
+    e2 = cudaMalloc(&c->U1, c->arr_elems * sizeof(double));
+    if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.stepper == MHD_RK3)
+      e2 = cudaMalloc(&c->U2, c->arr_elems * sizeof(double));
+  }
   cudaError_t e3 = cudaMalloc(&c->dbuf, 24 * sizeof(unsigned long long));
-  if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.stepper == MHD_RK3)
-    e2 = cudaMalloc(&c->U2, c->arr_elems * sizeof(double));
   if (e1 == cudaSuccess && e2 == cudaSuccess && c->scheme.ct) {
     e2 = cudaMalloc(&c->ctV, c->arr_elems * sizeof(double));
     for (int d = 0; d < 3 && e2 == cudaSuccess; ++d) e2 = cudaMalloc(&c->ctF[d], c->arr_elems * sizeof(double));
@@ -809,9 +929,6 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
     mhd_destroy(c);
     return MHD_E_CUDA;
   }
-  c->transport = dist ? dist->transport : MHD_TRANSPORT_NCCL;
-  if (const char* e = getenv("MHD_NCCL_SELF"))
-    c->nccl_self = atoi(e) == 1 && c->nranks == 1 && c->dim == 3 && c->bc_lo[2] == MHD_BC_PERIODIC;
   if (c->nranks > 1 || c->nccl_self) {  // the halo's stream and events (NCCL ranks and in-process slabs alike)
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
@@ -835,6 +952,15 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
       mhd_destroy(c);
       return MHD_E_NCCL;
     }
+  }
+  if (want_push && nccl_path) {
+    const int rc = push_setup_nccl(c);
+    if (rc) {
+      mhd_destroy(c);
+      return rc;
+    }
+  } else if (want_push && c->transport == MHD_TRANSPORT_LOCAL) {
+    c->push = true;  // (the neighbour slabs' arrays are bound by the group calls)
   }
   *out = c;
   return MHD_OK;
@@ -901,6 +1027,7 @@ int mhd_bind_workspace(mhd_ctx* c, void* dev_ptr, size_t bytes) {
     cudaGetLastError();
     return set_err(c, MHD_E_ARG, "workspace: not device memory of the context's device");
   }
+  if (c->nccl_mem) return set_err(c, MHD_E_STATE, "workspace: the state arrays are NCCL windows (MHD_HALO_PUSH)");
   CUDA_OR_RETURN(c, cudaStreamSynchronize(c->stream));
   WsArray a[10];
   const int n = ws_arrays(c, a);
@@ -911,6 +1038,7 @@ int mhd_bind_workspace(mhd_ctx* c, void* dev_ptr, size_t bytes) {
     p += ws_round(a[i].n);
   }
   c->borrowed = true;
+  c->push_valid = false;
   c->has_state = false;
   c->in_pending = false;
   c->ch_valid = false;
@@ -929,7 +1057,7 @@ int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
 int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
   if (!c || !U) return MHD_E_ARG;
   c->in_pending = false;  // supersedes a pending mhd_set_state_async
-  const size_t n = plane_elems(c) * (size_t)c->nzl;
+  c->push_valid = false;  const size_t n = plane_elems(c) * (size_t)c->nzl;
   c->sticky = MHD_OK;
   c->ch_valid = false;
   c->has_state = false;
@@ -1129,6 +1257,16 @@ int check_group(mhd_ctx* const* ctxs, int32_t n) {
     if (c->sticky != MHD_OK) return set_err(c, MHD_E_STATE, "context in error state %d", c->sticky);
     if (!c->has_state) return set_err(c, MHD_E_STATE, "no state set");
     c->group = ctxs;
+    if (c->push) {  // in-process halo push: the neighbour slabs' arrays
+      const mhd_ctx* dn = c->down >= 0 ? ctxs[c->down] : nullptr;
+      const mhd_ctx* up = c->up >= 0 ? ctxs[c->up] : nullptr;
+      if ((dn && !dn->push) || (up && !up->push)) return MHD_E_ARG;
+      for (int r = 0; r < 3; ++r) {
+        c->peer_dn[r] = dn ? (r == 0 ? dn->U0 : r == 1 ? dn->U1 : dn->U2) : nullptr;
+        c->peer_up[r] = up ? (r == 0 ? up->U0 : r == 1 ? up->U1 : up->U2) : nullptr;
+      }
+      c->peer_dn_nz = dn ? dn->nzl : 0;
+    }
     if (r > 0 && c->stream != ctxs[0]->stream) {  // one stream for the whole group
       if (c->own_stream && c->stream) {
         cudaStreamSynchronize(c->stream);
@@ -1237,13 +1375,18 @@ void mhd_destroy(mhd_ctx* c) {
   if (c->d2h) cudaStreamDestroy(c->d2h);
   for (cudaEvent_t e : {c->ev_in_copied, c->ev_in_free, c->ev_out_packed, c->ev_out_copied})
     if (e) cudaEventDestroy(e);
+  if (c->comm && !c->devcomm.empty()) mhd::devcomm_destroy(c->comm, c->devcomm.data());
+  for (int r = 0; r < 3; ++r)
+    if (c->comm && c->win[r]) ncclCommWindowDeregister(c->comm, c->win[r]);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
-  if (c->U0) cudaFree(c->U0);
-  if (c->U1) cudaFree(c->U1);
-  if (c->U2) cudaFree(c->U2);
+  for (double* u : {c->U0, c->U1, c->U2}) {
+    if (!u) continue;
+    if (c->nccl_mem) ncclMemFree(u);
+    else cudaFree(u);
+  }
   if (c->ctV) cudaFree(c->ctV);
   for (int d = 0; d < 3; ++d) {
     if (c->ctF[d]) cudaFree(c->ctF[d]);
@@ -1254,6 +1397,11 @@ void mhd_destroy(mhd_ctx* c) {
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
+}
+
+int mhd_halo_push(const mhd_ctx* c) {
+  if (!c) return MHD_E_ARG;
+  return c->push ? 1 : 0;
 }
 
 int mhd_profile_enable(mhd_ctx* c, int32_t enable) {

@@ -270,7 +270,7 @@ struct StageOcc {
 // so every warp runs at most 3 face solves per plane and the per-plane barriers do not wait
 // on a straggler.  Fluxes land in shared memory (Fz ping-pong, Fy, Fx); the update then forms
 // r = lx dFx + ly dFy + lz dFz (DESIGN.md §3.11 order).
-template <int DIM, int NV, int RS, int TY, int REC, bool TMA>
+template <int DIM, int NV, int RS, int TY, int REC, bool TMA, bool PUSH = false>
 __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)) k_stage(const __grid_constant__ StageArgs a) {
   // REC: reconstruction, a compile-time choice (0 PLM minmod, 1 PLM MC, 2 WENO-Z)
   constexpr bool WZ = REC == 2;
@@ -732,6 +732,19 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         if (NV > 8 && f == NV - 1 && a.last) v = v * c.damp;       // GLM damping once per step
         po[f * fs] = v;
       }
+      // halo push (the PUSH instances, 3D slabs; k is CTA-uniform, only boundary planes): the
+      // values just stored, read back through L2 (not forwarded from registers, which would hold
+      // them live across the loop) into the neighbours' ghost planes
+      if (PUSH && a.push_dn && k < a.gz) {
+        double* h = a.push_dn + (size_t)(a.push_dn_nz + a.gz + k) * pstride + own_cell;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) h[f * fs] = __ldcg(po + f * fs);
+      }
+      if (PUSH && a.push_up && k >= nzl - a.gz) {
+        double* h = a.push_up + (size_t)(k - (nzl - a.gz)) * pstride + own_cell;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) h[f * fs] = __ldcg(po + f * fs);
+      }
     }
     if constexpr (DIM == 3) {
       if (k + 1 < ke) {
@@ -964,12 +977,14 @@ template <int DIM, int NV, int RS, int TY, int REC>
 static cudaError_t launch_stage_t(const StageArgs& a0, cudaStream_t st) {
   using S = StageSmem<DIM, NV, TY, REC == 2 ? 3 : 2>;
   constexpr bool T = stage_tma<DIM, REC>();
-  auto kt = k_stage<DIM, NV, RS, TY, REC, T>;
-  auto kp = k_stage<DIM, NV, RS, TY, REC, false>;
+  constexpr bool P = DIM == 3;  // (the halo push exists for 3D slabs only)
   if (a0.ze <= a0.zb) return cudaSuccess;
   StageArgs a = a0;
   a.tma = T ? encode_window_map<NV>(a, S::PW, S::PH, (MHD_ZTMA && REC != 2) ? TY : 0) : 0;
-  auto kern = a.tma ? kt : kp;
+  // the PUSH instances only when this launch pushes: the others carry no trace of it
+  const bool push = P && (a.push_dn || a.push_up);
+  auto kern = a.tma ? (push ? k_stage<DIM, NV, RS, TY, REC, T, P> : k_stage<DIM, NV, RS, TY, REC, T, false>)
+                    : (push ? k_stage<DIM, NV, RS, TY, REC, false, P> : k_stage<DIM, NV, RS, TY, REC, false, false>);
   // (the attribute is per device: set on every launch, a host-side call of ~1 us)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   if (e != cudaSuccess) return e;

@@ -37,6 +37,14 @@ struct StageArgs {
   StageConsts c;
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
   unsigned long long* bad;       // [4] lowest bad global linear index per stage (0 = dt pass)
+  // halo push (3D slabs, MHD_HALO_PUSH): the z neighbours' arrays of Uout's role (storage plane
+  // 0; peer memory: an NCCL symmetric window or an in-process slab), null where there is none.
+  // Interior plane m < gz is also stored to the down neighbour's top ghost plane
+  // push_dn_nz + gz + m, plane m >= nz_loc - gz to the up neighbour's bottom ghost plane
+  // m - (nz_loc - gz): the next stage's z halo, written by this stage's epilogue
+  double* push_dn;
+  double* push_up;
+  int push_dn_nz;
 };
 
 struct DtArgs {
@@ -92,6 +100,13 @@ cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStr
                                cudaStream_t aux2, cudaEvent_t* ev);
 inline int split_row_pitch(int nx) { return (nx + 1 + 31) / 32 * 32; }
 cudaError_t launch_ct_dt(const DtArgs& a, int nsm, cudaStream_t st);
+// halo push over NCCL symmetric windows (mhd_push.cu); win: ncclWindow_t of U0, U1, U2 (or null)
+cudaError_t push_peer_pointers(void* const win[3], int down, int up, double* out[6], cudaStream_t st);
+cudaError_t push_barrier(const void* devcomm, cudaStream_t st);
+size_t devcomm_bytes();
+int devcomm_create(void* comm, void* out);
+void devcomm_destroy(void* comm, const void* dc);
+int lsa_team_size(void* comm);
 int stage_tile_rows(int dim, int limiter);
 int stage_ctas_per_sm(int dim, int nv, int riemann, int limiter);  // resident CTAs per SM of the stage kernel
 cudaError_t launch_dt(int dim, int nv, const DtArgs& a, int nsm, cudaStream_t st);

@@ -30,7 +30,8 @@ EXPORTS = ("mhd_nccl_get_unique_id", "mhd_create", "mhd_set_stream", "mhd_local_
            "mhd_destroy", "mhd_debug_face_flux", "mhd_profile_enable", "mhd_profile_read", "mhd_version",
            "mhd_group_compute_dt", "mhd_group_step", "mhd_halo_plan", "mhd_debug_fast_ops",
            "mhd_get_state_box", "mhd_set_state_async", "mhd_get_state_async", "mhd_io_join",
-           "mhd_workspace_bytes", "mhd_bind_workspace", "mhd_run", "mhd_profile_read_stages")
+           "mhd_workspace_bytes", "mhd_bind_workspace", "mhd_run", "mhd_profile_read_stages",
+           "mhd_halo_push")
 TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1
 
 
@@ -112,6 +113,8 @@ def load() -> C.CDLL:
     L.mhd_profile_enable.argtypes = [P, C.c_int32]
     L.mhd_profile_read.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.mhd_profile_read_stages.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    if hasattr(L, "mhd_halo_push"):  # (older A/B builds lack it)
+        L.mhd_halo_push.argtypes = [P]
     L.mhd_group_compute_dt.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(C.c_double)]
     L.mhd_group_step.argtypes = [C.POINTER(P), C.c_int32, C.c_double]
     L.mhd_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
@@ -314,6 +317,12 @@ class Solver:
         self._check(self._L.mhd_profile_read_stages(self._h, ms, n))
         return {"dt": (ms[0], n[0]), "stage1": (ms[1], n[1]), "stage2": (ms[2], n[2]), "stage3": (ms[3], n[3]),
                 "halo_exposed": (ms[4], n[4])}
+
+    @property
+    def halo_push(self) -> bool:
+        """True if this context's stages push their boundary planes to the z neighbours
+        (MHD_HALO_PUSH=1 at creation, include/mhd.h mhd_halo_push)."""
+        return hasattr(self._L, "mhd_halo_push") and self._L.mhd_halo_push(self._h) == 1
 
     def destroy(self) -> None:
         if getattr(self, "_h", None):

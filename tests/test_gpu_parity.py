@@ -1061,3 +1061,95 @@ def test_nccl_self_exchange_bitwise(mhd, scheme):
         assert d1[k] == dN[k]
     if scheme == "plm-rk2":  # the fused stage ran the split schedule (one exposed-halo pair per stage)
         assert prof["halo_exposed"][1] == 8
+
+
+def _with_env(env, make):
+    """construct under extra environment variables (read by mhd_create), then restore"""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return make()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["plm-P2", "plm-P3", "plm-P4", "plm-P8", "rk3-P4", "wenoz-fused-P3", "outflow-P4"])
+def test_halo_push_slab_group_bitwise(mhd, case):
+    """MHD_HALO_PUSH=1 (include/mhd.h mhd_halo_push): each fused stage's epilogue also stores its
+    g boundary planes into the neighbour slabs' ghost planes of the next stage's input, and every
+    stage after the first runs as one launch with no exchange.  Bitwise equal to one domain with
+    equal counters, also across a state change in the middle of the run (the next stage
+    exchanges again); P = 8: 4-plane slabs, every plane a boundary plane."""
+    scheme, P = case.rsplit("-P", 1)
+    P = int(P)
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 30 if P == 3 else 32))
+    env = {"MHD_HALO_PUSH": "1"}
+    if scheme == "rk3":
+        p = p.replace(stepper=I.RK3)
+    if scheme == "wenoz-fused":
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+        env["MHD_FUSED_WENOZ"] = "1"
+    if scheme == "outflow":
+        p = p.replace(bc=(I.PERIODIC, I.PERIODIC, I.OUTFLOW))
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    U0b = I.with_noise(I.orszag_tang_3d_ic(p), p, seed=7)
+    s = _with_env({k: v for k, v in env.items() if k != "MHD_HALO_PUSH"}, lambda: mhd.Solver(p))
+    s.set_state(U0)
+    log1 = list(s.run(3))
+    s.set_state(U0b)
+    log1 += list(s.run(3))
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    g = _with_env(env, lambda: mhd.SolverGroup(p, P))
+    assert all(sl.halo_push for sl in g.slabs)
+    g.set_state(U0)
+    logP = list(g.run(3))
+    for sl in g.slabs:
+        sl.profile_enable(True, capacity=64)
+    g.set_state(U0b)
+    logP += list(g.run(3))
+    prof = [sl.profile_read_stages() for sl in g.slabs]
+    UP, dP = g.get_state(), g.diag()
+    g.destroy()
+    assert np.array_equal(np.array(log1), np.array(logP))
+    assert np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k]
+    # after the state change only the first stage waited for an exchange
+    assert all(pr["halo_exposed"][1] == 1 for pr in prof)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme", ["plm-rk2", "plm-rk3"])
+def test_halo_push_nccl_windows_self_bitwise(mhd, scheme):
+    """The NCCL halo push on one GPU (MHD_NCCL_SELF=1 MHD_HALO_PUSH=1): the state arrays are NCCL
+    symmetric windows of a one-rank communicator, the periodic z neighbour's window address comes
+    from ncclGetPeerPointer, the stage epilogue stores the boundary planes through it and an LSA
+    barrier kernel follows each stage — bitwise equal to one domain, with one exchange (the first
+    stage) in the whole run."""
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
+    if scheme == "plm-rk3":
+        p = p.replace(stepper=I.RK3)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(5)
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    s = _with_env({"MHD_NCCL_SELF": "1", "MHD_HALO_PUSH": "1"}, lambda: mhd.Solver(p))
+    assert s.halo_push
+    s.set_state(U0)
+    s.profile_enable(True, capacity=64)
+    logN = s.run(5)
+    prof = s.profile_read_stages()
+    UN, dN = s.get_state(), s.diag()
+    s.destroy()
+    assert np.array_equal(log1, logN) and np.array_equal(U1, UN)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dN[k]
+    assert prof["halo_exposed"][1] == 1

@@ -4,7 +4,9 @@ N ranks, one GPU each, every case runs the real multi-rank path of libmhd — NC
 on the comm stream overlapped with the interior launch, ncclAllReduce for dt, counters and bad
 cells (mhd_api.cu fused_stage / whole_fill_ghosts / reduce_and_read) — and each rank compares its
 slab with the same problem run as one domain on its own GPU: dt log and state bitwise, global
-counters equal.  Rank 0 writes the results as JSON (--out).
+counters equal.  The "-push" cases run the halo push instead (MHD_HALO_PUSH=1: boundary planes
+stored by the stage epilogue into the neighbours' NCCL symmetric windows, an LSA barrier per
+stage).  Rank 0 writes the results as JSON (--out).
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/nccl_parity.py --out r.json
 """
@@ -33,6 +35,12 @@ def cases(I, world):
     yield "blast-weak", b, I.blast_3d_ic(b)
     o = ot.replace(bc=(I.PERIODIC, I.PERIODIC, I.OUTFLOW))
     yield "ot3d-outflow-z", o, I.with_noise(I.orszag_tang_3d_ic(o), o)
+    # the halo push over NCCL symmetric windows (MHD_HALO_PUSH=1; fused stages only)
+    yield "ot3d-plm-rk2-push", ot, I.with_noise(I.orszag_tang_3d_ic(ot), ot)
+    r3 = ot.replace(stepper=I.RK3)
+    yield "ot3d-plm-rk3-push", r3, I.with_noise(I.orszag_tang_3d_ic(r3), r3)
+    yield "blast-weak-push", b, I.blast_3d_ic(b)
+    yield "ot3d-outflow-z-push", o, I.with_noise(I.orszag_tang_3d_ic(o), o)
 
 
 def main():
@@ -58,8 +66,15 @@ def main():
         s1.destroy()
         obj = [mhd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        s = mhd.Solver(p, rank=rank, nranks=world, device=local, nccl_id=obj[0])
+        push = name.endswith("-push")
+        if push:
+            os.environ["MHD_HALO_PUSH"] = "1"
+        try:
+            s = mhd.Solver(p, rank=rank, nranks=world, device=local, nccl_id=obj[0])
+        finally:
+            os.environ.pop("MHD_HALO_PUSH", None)
         z0, nz = s.offset[2], s.extent[2]
+        pushed = s.halo_push
         s.set_state(np.ascontiguousarray(U0[:, z0:z0 + nz]))
         logP = s.run(args.steps)
         UP, dP = s.get_state(), s.diag()
@@ -69,7 +84,7 @@ def main():
         flag = torch.tensor([1 if ok else 0], device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         res.append({"case": name, "bitwise": bool(flag.item()), "global": list(p.n), "ranks": world,
-                    "steps": args.steps})
+                    "steps": args.steps, **({"halo_push_active": pushed} if push else {})})
     if rank == 0:
         line = json.dumps({"cases": res})
         print(line, flush=True)

@@ -7,6 +7,7 @@ after the interior (class 4).  Prints one JSON line per P.  Under torchrun, benc
 same quantity for the NCCL transport ("halo_exposed_ms_per_step").
 
   python tools/slab_overlap.py --n 256 --P 2 4 8
+  MHD_HALO_PUSH=1 python tools/slab_overlap.py ...   the halo pushed by each stage's epilogue
 """
 import argparse
 import json
@@ -58,7 +59,10 @@ def main():
                           "stage_ms_per_step_sum_over_slabs": stages / args.steps,
                           "halo_exposed_ms_per_step_sum_over_slabs": halo / args.steps,
                           "halo_exposed_share_of_stage_time": halo / max(stages, 1e-9),
-                          "transport": "in-process device copies (MHD_TRANSPORT_LOCAL), one GPU"}), flush=True)
+                          "halo_push": g.slabs[0].halo_push,
+                          "transport": ("in-process halo push from the stage epilogue (MHD_HALO_PUSH=1)"
+                                        if g.slabs[0].halo_push else
+                                        "in-process device copies (MHD_TRANSPORT_LOCAL)") + ", one GPU"}), flush=True)
         g.destroy()
 
 
