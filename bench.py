@@ -550,9 +550,9 @@ def main():
     # launches with slabs: interior and the two boundary ranges), or five launches for CT and for
     # the 3D GLM WENO-Z split stage (mhd_split.cu; MHD_FUSED_WENOZ=1 selects the fused kernel)
     split = (p.limiter == I.WENOZ and p.n[2] > 1 and not p.ct and os.environ.get("MHD_FUSED_WENOZ") != "1")
-    # (halo push: the stage launch and the LSA barrier kernel)
+    # (halo push: the stage's launches and the LSA barrier kernel)
     slabs = world > 1 or os.environ.get("MHD_NCCL_SELF") == "1"  # (one-rank NCCL slab: the slab schedule)
-    launches_per_stage = 5 if (p.ct or split) else (2 if push else 3 if slabs else 1)
+    launches_per_stage = (5 + push) if (p.ct or split) else (2 if push else 3 if slabs else 1)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

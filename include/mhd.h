@@ -250,10 +250,10 @@ int mhd_profile_read(mhd_ctx* ctx, double ms[2], int64_t launches[2]);
 int mhd_profile_read_stages(mhd_ctx* ctx, double ms[5], int64_t units[5]);
 
 /* Halo push (the z halo of each RK stage).  With the
- * environment variable MHD_HALO_PUSH=1 at mhd_create, a 3D slab context of the fused stage
- * (PLM or fused WENO-Z, GLM; not CT, not the split WENO-Z stage) has each stage's epilogue store
+ * environment variable MHD_HALO_PUSH=1 at mhd_create, a 3D slab context has each stage's last
+ * kernel (the fused stage kernel; the update kernel of the split WENO-Z and CT stages) store
  * its g boundary planes also into the z neighbours' ghost planes of the next stage's input, so
- * the next stage runs as one launch with no exchange.  NCCL ranks: the state arrays are NCCL
+ * the next stage needs no exchange (the fused stage then runs as one launch).  NCCL ranks: the state arrays are NCCL
  * symmetric windows (ncclMemAlloc, ncclCommWindowRegister; every neighbour must be reachable
  * by load/store, i.e. on the same node), and a one-CTA NCCL LSA barrier after every pushing
  * stage orders the ranks; the set-up is agreed over all ranks, and if any step of it fails on

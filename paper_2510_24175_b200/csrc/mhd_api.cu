@@ -152,10 +152,10 @@ bool nccl_active(const mhd_ctx* c) {
 }
 // the role (0 U^n, 1 U*/U1, 2 U2) of one of the context's state arrays
 int role_of(const mhd_ctx* c, const double* p) { return p == c->U0 ? 0 : p == c->U1 ? 1 : 2; }
-// MHD_HALO_PUSH=1 asks for the halo push; it applies to the fused 3D stages on slabs
+// MHD_HALO_PUSH=1 asks for the halo push (3D slabs: the fused, split WENO-Z and CT stages)
 bool push_requested(const mhd_ctx* c) {
   const char* e = getenv("MHD_HALO_PUSH");
-  return e && atoi(e) == 1 && c->dim == 3 && !c->scheme.ct && !c->split && (c->nranks > 1 || c->nccl_self);
+  return e && atoi(e) == 1 && c->dim == 3 && (c->nranks > 1 || c->nccl_self);
 }
 
 // Host wait for the context's stream.  With NCCL slabs the stream may wait on collectives of
@@ -390,11 +390,23 @@ void prof_drain(mhd_ctx* c) {
 int whole_fill_ghosts(mhd_ctx* c, int stage) {
   int rc = fill_z_ghosts_local(c, stage_plan(c, stage).in);
   if (rc) return rc;
-  if (slabbed(c)) {
+  if (slabbed(c) && !(c->push && c->push_valid)) {  // (pushed: the neighbours stored them already)
     if ((rc = exchange(c, stage))) return rc;
     CUDA_OR_RETURN(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
   }
   return MHD_OK;
+}
+
+// the halo-push pointers of a launch writing `out` (null when the context does not push)
+template <typename Args>
+void set_push(const mhd_ctx* c, const double* out, Args& a) {
+  a.push_dn = a.push_up = nullptr;
+  a.push_dn_nz = 0;
+  if (!c->push) return;
+  const int r = role_of(c, out);
+  a.push_dn = c->peer_dn[r];
+  a.push_up = c->peer_up[r];
+  a.push_dn_nz = c->peer_dn_nz;
 }
 
 int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
@@ -424,14 +436,7 @@ int run_stage(mhd_ctx* c, int stage, const StageConsts& k, int zb, int ze) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
-  a.push_dn = a.push_up = nullptr;
-  a.push_dn_nz = 0;
-  if (c->push) {  // this stage's boundary planes also go to the neighbours' ghost planes of sp.out
-    const int r = role_of(c, sp.out);
-    a.push_dn = c->peer_dn[r];
-    a.push_up = c->peer_up[r];
-    a.push_dn_nz = c->peer_dn_nz;
-  }
+  set_push(c, sp.out, a);  // the boundary planes also to the neighbours' ghost planes of sp.out
   cudaError_t e = mhd::launch_stage(c->dim, c->nv, c->scheme.riemann, a, c->stream);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "stage %d launch: %s", stage, cudaGetErrorString(e));
   return MHD_OK;
@@ -528,11 +533,14 @@ int run_ct_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
+  set_push(c, sp.out, a);  // (the update kernel's epilogue)
   const int pr = prof_begin(c, stage);
   if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_ct_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
-  prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "ct stage %d: %s", stage, cudaGetErrorString(e));
+  if (c->push)
+    if (int rc = push_fence(c)) return rc;
+  prof_end(c, pr);
   return MHD_OK;
 }
 
@@ -564,11 +572,14 @@ int run_split_stage(mhd_ctx* c, int stage, const StageConsts& k) {
   a.c = k;
   a.counters = c->dbuf + 2;
   a.bad = c->dbuf + 5;
+  set_push(c, sp.out, a);  // (the update kernel's epilogue)
   const int pr = prof_begin(c, stage);
   if (int rc_aux = aux_streams(c)) return rc_aux;
   cudaError_t e = mhd::launch_split_stage(c->scheme.riemann, a, c->nsm, c->stream, c->sp_aux[0], c->sp_aux[1], c->sp_ev);
-  prof_end(c, pr);
   if (e != cudaSuccess) return set_err(c, MHD_E_CUDA, "split stage %d: %s", stage, cudaGetErrorString(e));
+  if (c->push)
+    if (int rc = push_fence(c)) return rc;
+  prof_end(c, pr);
   return MHD_OK;
 }
 

@@ -74,6 +74,9 @@ struct CtArgs {
   StageConsts c;
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
   unsigned long long* bad;       // [4] per stage
+  double* push_dn;               // halo push, as in StageArgs (null: none)
+  double* push_up;
+  int push_dn_nz;
 };
 cudaError_t launch_ct_stage(int riemann, const CtArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
                             cudaStream_t aux2, cudaEvent_t* ev);
@@ -95,6 +98,9 @@ struct SplitArgs {
   StageConsts c;
   unsigned long long* counters;  // [p_floors, plm_fallbacks, hlld_to_hll]
   unsigned long long* bad;       // [4] per stage
+  double* push_dn;               // halo push, as in StageArgs (null: none)
+  double* push_up;
+  int push_dn_nz;
 };
 cudaError_t launch_split_stage(int riemann, const SplitArgs& a, int nsm, cudaStream_t st, cudaStream_t aux1,
                                cudaStream_t aux2, cudaEvent_t* ev);

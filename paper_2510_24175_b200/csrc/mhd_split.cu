@@ -248,6 +248,18 @@ __global__ void __launch_bounds__(256) k_sp_update(SplitArgs a) {
     if (a.last) v[NVS - 1] = v[NVS - 1] * a.c.damp;  // GLM damping once per step
 #pragma unroll
     for (int f = 0; f < NVS; ++f) po[f * fs] = v[f];
+    // halo push: a boundary plane also into the z neighbour's ghost plane
+    const size_t cell = (size_t)j * a.nx + i;
+    if (a.push_dn && k < a.gz) {
+      double* h = a.push_dn + (size_t)(a.push_dn_nz + a.gz + k) * X.ps + cell;
+#pragma unroll
+      for (int f = 0; f < NVS; ++f) h[f * fs] = v[f];
+    }
+    if (a.push_up && k >= a.nz - a.gz) {
+      double* h = a.push_up + (size_t)(k - (a.nz - a.gz)) * X.ps + cell;
+#pragma unroll
+      for (int f = 0; f < NVS; ++f) h[f * fs] = v[f];
+    }
   }
 }
 

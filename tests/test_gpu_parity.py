@@ -1125,7 +1125,7 @@ def test_halo_push_slab_group_bitwise(mhd, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scheme", ["plm-rk2", "plm-rk3"])
+@pytest.mark.parametrize("scheme", ["plm-rk2", "plm-rk3", "wenoz-rk3", "ct-rk2"])
 def test_halo_push_nccl_windows_self_bitwise(mhd, scheme):
     """The NCCL halo push on one GPU (MHD_NCCL_SELF=1 MHD_HALO_PUSH=1): the state arrays are NCCL
     symmetric windows of a one-rank communicator, the periodic z neighbour's window address comes
@@ -1135,7 +1135,12 @@ def test_halo_push_nccl_windows_self_bitwise(mhd, scheme):
     p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
     if scheme == "plm-rk3":
         p = p.replace(stepper=I.RK3)
-    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    if scheme == "wenoz-rk3":  # the split stage: the push from k_sp_update
+        p = p.replace(limiter=I.WENOZ, stepper=I.RK3)
+    if scheme == "ct-rk2":  # the push from k_ct_update (and the CT dt pass reads the pushed planes)
+        p = I.ct_problem(I.orszag_tang_3d(16))
+    U0 = I.orszag_tang_3d_ic(p.replace(ct=0, glm=1) if p.ct else p)
+    U0 = np.ascontiguousarray(U0[:8] if p.ct else I.with_noise(U0, p))
     s = mhd.Solver(p)
     s.set_state(U0)
     log1 = s.run(5)
@@ -1152,4 +1157,46 @@ def test_halo_push_nccl_windows_self_bitwise(mhd, scheme):
     assert np.array_equal(log1, logN) and np.array_equal(U1, UN)
     for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
         assert d1[k] == dN[k]
-    assert prof["halo_exposed"][1] == 1
+    if scheme.startswith("plm"):  # (the fused stage's split schedule ran once)
+        assert prof["halo_exposed"][1] == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["wenoz-split-P2", "wenoz-split-P4", "ct-plm-P4", "ct-wenoz-P3"])
+def test_halo_push_split_and_ct_bitwise(mhd, case):
+    """The halo push from the update kernels of the split WENO-Z stage (mhd_split.cu k_sp_update)
+    and the CT stage (mhd_ct.cu k_ct_update): the next stage (and the CT dt pass, which reads
+    B_z of the ghost plane) skips its exchange.  Bitwise equal to one domain with equal counters,
+    across a state change; only the first stage after each state change exchanges."""
+    from test_oracle_scheme import _random_ct_state
+    scheme, P = case.rsplit("-P", 1)
+    P = int(P)
+    if scheme == "wenoz-split":
+        p = I.orszag_tang_3d(32).replace(n=(40, 21, 24), limiter=I.WENOZ, stepper=I.RK3)
+        U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+        U0b = I.with_noise(I.orszag_tang_3d_ic(p), p, seed=7)
+    else:
+        lim = I.MC if scheme == "ct-plm" else I.WENOZ
+        p = I.orszag_tang_3d(12, limiter=lim).replace(n=(20, 14, 24), ct=1, glm=0,
+                                                       stepper=I.RK2 if lim == I.MC else I.RK3)
+        U0 = _random_ct_state(p)
+        U0b = _random_ct_state(p, seed=11)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = list(s.run(3))
+    s.set_state(U0b)
+    log1 += list(s.run(3))
+    U1, d1 = s.get_state(), s.diag()
+    s.destroy()
+    g = _with_env({"MHD_HALO_PUSH": "1"}, lambda: mhd.SolverGroup(p, P))
+    assert all(sl.halo_push for sl in g.slabs)
+    g.set_state(U0)
+    logP = list(g.run(3))
+    g.set_state(U0b)
+    logP += list(g.run(3))
+    UP, dP = g.get_state(), g.diag()
+    g.destroy()
+    assert np.array_equal(np.array(log1), np.array(logP))
+    assert np.array_equal(U1, UP)
+    for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
+        assert d1[k] == dP[k]
