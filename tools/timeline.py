@@ -79,10 +79,12 @@ def main():
     iv = intervals(trace)
     stages = [e for e in iv if "k_stage" in e["name"]]
     halo = [e for e in iv if "nccl" in e["name"].lower() or e["cat"] == "gpu_memcpy"]
+    barriers = [e["end"] - e["ts"] for e in iv if "k_push_barrier" in e["name"]]  # (MHD_HALO_PUSH)
     summary = {"n": args.n, "slabs": args.slabs, "ranks": world, "rank": rank, "steps": args.steps,
                "nccl_self": os.environ.get("MHD_NCCL_SELF") == "1",
                "stage_launches": len(stages), "halo_events": len(halo),
-               "kernels": sorted({e["name"][:60] for e in iv}), "stages": []}
+               "kernels": sorted({e["name"][:60] for e in iv}), "stages": [],
+               "push_barrier_us": barriers}
     # per stage: the long (interior) launch and the halo events that ran beside it
     for s in stages:
         if s["end"] - s["ts"] < 0.25 * max(x["end"] - x["ts"] for x in stages):
