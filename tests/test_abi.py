@@ -79,6 +79,8 @@ def test_create_rejects_bad_arguments_without_gpu(lib):
     assert h.value is None
     assert lib.mhd_create(None, 5 / 3, 0.4, None, None, None, C.byref(h)) == mhd.MHD_E_ARG
     lib.mhd_destroy(None)  # NULL-safe
+    lib.mhd_halo_push.argtypes = [C.c_void_p]
+    assert lib.mhd_halo_push(None) == mhd.MHD_E_ARG
 
 
 def test_product_package_does_not_import_the_oracle():
