@@ -71,12 +71,13 @@ struct mhd_ctx {
   cudaStream_t comm_stream = nullptr;            // NCCL halo exchange (overlaps the interior)
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   mhd_ctx* const* group = nullptr;                // MHD_TRANSPORT_LOCAL: the slabs of this group
-  // halo push (MHD_HALO_PUSH=1; 3D fused stages on slabs): each stage's epilogue stores its g
-  // boundary planes into the z neighbours' ghost planes of the next stage's input, so the next
-  // stage needs no exchange and runs as one launch (§8).  NCCL ranks: the arrays are symmetric
-  // windows, the peers' arrays plain pointers into NVLink peer memory, and a one-CTA LSA
-  // barrier after each pushing stage orders the ranks; in-process slabs: the peer slabs'
-  // arrays, one stream.
+  // halo push (MHD_HALO_PUSH=1; 3D slabs): each stage's last kernel stores its g boundary
+  // planes into the z neighbours' ghost planes of the next stage's input, so the next stage
+  // needs no exchange (the fused stage runs as one launch; §8).  NCCL ranks: the arrays are
+  // symmetric windows, the peers' arrays plain pointers into NVLink peer memory, and a one-CTA
+  // LSA barrier after each pushing stage orders the ranks (a state change must then be made on
+  // every rank, as every caller here does); in-process slabs: the peer slabs' arrays, one
+  // stream, and a state change of any slab invalidates the pushed planes of all (check_group).
   bool push = false;                              // the transport is set up for pushing
   bool push_valid = false;                        // the next stage's input ghost planes were pushed
   double* peer_dn[3] = {nullptr, nullptr, nullptr};  // down / up neighbour's U0, U1, U2
@@ -1068,7 +1069,8 @@ int mhd_device_bytes(const mhd_ctx* c, size_t* bytes) {
 int mhd_set_state(mhd_ctx* c, const double* U, int32_t on_device) {
   if (!c || !U) return MHD_E_ARG;
   c->in_pending = false;  // supersedes a pending mhd_set_state_async
-  c->push_valid = false;  const size_t n = plane_elems(c) * (size_t)c->nzl;
+  c->push_valid = false;
+  const size_t n = plane_elems(c) * (size_t)c->nzl;
   c->sticky = MHD_OK;
   c->ch_valid = false;
   c->has_state = false;
@@ -1272,9 +1274,9 @@ int check_group(mhd_ctx* const* ctxs, int32_t n) {
       const mhd_ctx* dn = c->down >= 0 ? ctxs[c->down] : nullptr;
       const mhd_ctx* up = c->up >= 0 ? ctxs[c->up] : nullptr;
       if ((dn && !dn->push) || (up && !up->push)) return MHD_E_ARG;
-      for (int r = 0; r < 3; ++r) {
-        c->peer_dn[r] = dn ? (r == 0 ? dn->U0 : r == 1 ? dn->U1 : dn->U2) : nullptr;
-        c->peer_up[r] = up ? (r == 0 ? up->U0 : r == 1 ? up->U1 : up->U2) : nullptr;
+      for (int q = 0; q < 3; ++q) {
+        c->peer_dn[q] = dn ? (q == 0 ? dn->U0 : q == 1 ? dn->U1 : dn->U2) : nullptr;
+        c->peer_up[q] = up ? (q == 0 ? up->U0 : q == 1 ? up->U1 : up->U2) : nullptr;
       }
       c->peer_dn_nz = dn ? dn->nzl : 0;
     }
@@ -1287,6 +1289,11 @@ int check_group(mhd_ctx* const* ctxs, int32_t n) {
       c->own_stream = false;
     }
   }
+  // pushed ghost planes are valid only if no slab's state changed since the last pushing stage
+  // (a slab's new interior planes are its neighbours' ghosts): all or none
+  bool valid = true;
+  for (int r = 0; r < n; ++r) valid = valid && ctxs[r]->push_valid;
+  for (int r = 0; r < n; ++r) ctxs[r]->push_valid = valid;
   return MHD_OK;
 }
 }  // namespace

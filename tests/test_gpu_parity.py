@@ -1200,3 +1200,33 @@ def test_halo_push_split_and_ct_bitwise(mhd, case):
     assert np.array_equal(U1, UP)
     for k in ("p_floors", "plm_fallbacks", "hlld_to_hll"):
         assert d1[k] == dP[k]
+
+
+@pytest.mark.gpu
+def test_halo_push_one_slab_state_change(mhd):
+    """A state change of ONE slab of a pushing group (its new boundary planes are its neighbours'
+    ghost planes): the group falls back to the exchange for the next stage on every slab, and
+    the run equals one domain given the same spliced state, bitwise."""
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 32))
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    U0b = I.with_noise(I.orszag_tang_3d_ic(p), p, seed=7)
+    g = _with_env({"MHD_HALO_PUSH": "1"}, lambda: mhd.SolverGroup(p, 4))
+    g.set_state(U0)
+    logP = list(g.run(2))
+    Umid = g.get_state()
+    sl = g.slabs[1]
+    z0, nz = sl.offset[2], sl.extent[2]
+    sl.set_state(np.ascontiguousarray(U0b[:, z0:z0 + nz]))
+    logP += list(g.run(3))
+    UP = g.get_state()
+    g.destroy()
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = list(s.run(2))
+    assert np.array_equal(s.get_state(), Umid)
+    Umid[:, z0:z0 + nz] = U0b[:, z0:z0 + nz]
+    s.set_state(np.ascontiguousarray(Umid))
+    log1 += list(s.run(3))
+    U1 = s.get_state()
+    s.destroy()
+    assert np.array_equal(np.array(log1), np.array(logP)) and np.array_equal(U1, UP)
