@@ -257,7 +257,8 @@ int mhd_profile_read_stages(mhd_ctx* ctx, double ms[5], int64_t units[5]);
  * symmetric windows (ncclMemAlloc, ncclCommWindowRegister; every neighbour must be reachable
  * by load/store, i.e. on the same node), and a one-CTA NCCL LSA barrier after every pushing
  * stage orders the ranks; the set-up is agreed over all ranks, and if any step of it fails on
- * any rank no rank pushes (the send/recv exchange stays in use).  In-process slab groups: the
+ * any rank no rank pushes (the send/recv exchange stays in use; MHD_HALO_PUSH_FAULT=1..4 injects
+ * such a failure, for tests).  In-process slab groups: the
  * neighbour slabs' arrays.  The first stage after a state change (mhd_set_state*,
  * mhd_bind_workspace) exchanges as before.  Results are bitwise those of the exchange.
  * Returns 1 if the context pushes, 0 if not, MHD_E_ARG for a null context.  With pushing NCCL

@@ -704,25 +704,31 @@ int agree(mhd_ctx* c, int ok) {
 // memory; the rank itself for MHD_NCCL_SELF).  Every step is agreed over the ranks, so either
 // all push or none does (then the send/recv exchange is used and the windows are released).
 int push_setup_nccl(mhd_ctx* c) {
-  int ok = agree(c, mhd::lsa_team_size(c->comm) == c->nranks);  // every neighbour load/store-accessible
+  // MHD_HALO_PUSH_FAULT=k (tests): step k of the set-up fails on this rank (1 the LSA check,
+  // 2 the second window, 3 the device communicator, 4 the peer pointers)
+  const char* fe = getenv("MHD_HALO_PUSH_FAULT");
+  const int fault = fe ? atoi(fe) : 0;
+  int ok = agree(c, mhd::lsa_team_size(c->comm) == c->nranks && fault != 1);  // neighbours load/store-accessible
   double* arr[3] = {c->U0, c->U1, c->U2};
   for (int r = 0; r < 3 && ok; ++r) {
     if (!arr[r]) continue;
-    const int mine = ncclCommWindowRegister(c->comm, arr[r], c->nccl_mem_bytes, &c->win[r], NCCL_WIN_COLL_SYMMETRIC) ==
-                     ncclSuccess;
+    const int mine = !(fault == 2 && r == 1) &&
+                     ncclCommWindowRegister(c->comm, arr[r], c->nccl_mem_bytes, &c->win[r], NCCL_WIN_COLL_SYMMETRIC) ==
+                         ncclSuccess;
     if (!mine) c->win[r] = nullptr;
     ok = agree(c, mine);
   }
   if (ok) {
     c->devcomm.assign(mhd::devcomm_bytes(), 0);
-    ok = agree(c, mhd::devcomm_create(c->comm, c->devcomm.data()) == 0);
-    if (!ok) c->devcomm.clear();
+    const bool made = fault != 3 && mhd::devcomm_create(c->comm, c->devcomm.data()) == 0;
+    if (!made) c->devcomm.clear();
+    ok = agree(c, made);  // (a communicator made here but not elsewhere is destroyed below)
   }
   if (ok) {
     double* p[6];
     void* w[3] = {c->win[0], c->win[1], c->win[2]};
     const int dn = c->nccl_self ? 0 : c->down, up = c->nccl_self ? 0 : c->up;
-    ok = agree(c, mhd::push_peer_pointers(w, dn, up, p, c->stream) == cudaSuccess);
+    ok = agree(c, fault != 4 && mhd::push_peer_pointers(w, dn, up, p, c->stream) == cudaSuccess);
     for (int r = 0; r < 3 && ok; ++r) {
       c->peer_dn[r] = p[2 * r];
       c->peer_up[r] = p[2 * r + 1];

@@ -1230,3 +1230,26 @@ def test_halo_push_one_slab_state_change(mhd):
     U1 = s.get_state()
     s.destroy()
     assert np.array_equal(np.array(log1), np.array(logP)) and np.array_equal(U1, UP)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fault", [1, 2, 3, 4])
+def test_halo_push_setup_failure_falls_back(mhd, fault):
+    """A failed step of the NCCL halo-push set-up (injected by MHD_HALO_PUSH_FAULT: the LSA check,
+    a window registration, the device communicator, the peer pointers) releases what was set up
+    and leaves the context on the send/recv exchange: no push, bitwise the same run."""
+    p = I.orszag_tang_3d(32).replace(n=(40, 21, 32), stepper=I.RK3)
+    U0 = I.with_noise(I.orszag_tang_3d_ic(p), p)
+    s = mhd.Solver(p)
+    s.set_state(U0)
+    log1 = s.run(3)
+    U1 = s.get_state()
+    s.destroy()
+    s = _with_env({"MHD_NCCL_SELF": "1", "MHD_HALO_PUSH": "1", "MHD_HALO_PUSH_FAULT": str(fault)},
+                  lambda: mhd.Solver(p))
+    assert not s.halo_push
+    s.set_state(U0)
+    logN = s.run(3)
+    UN = s.get_state()
+    s.destroy()
+    assert np.array_equal(log1, logN) and np.array_equal(U1, UN)
