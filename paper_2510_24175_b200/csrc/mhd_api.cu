@@ -878,7 +878,7 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
   // z chunk per CTA (3D): the CTAs of one stage launch run in waves of nsm x (resident CTAs
   // per SM); a chunk of kz planes costs ~kz + 1.5 plane-times (the prologue solves one extra z
   // face and converts 2 extra planes).  Pick the chunk count minimising waves x chunk cost
-  // (MHD_KZ overrides, for measurements).
+  // (small grids: enough CTAs to fill the GPU), ... (MHD_KZ overrides, for measurements).
   {
     const int ty = mhd::stage_tile_rows(c->dim, c->scheme.limiter);
     const long long tiles = (long long)((c->nx + 31) / 32) * ((c->ny + ty - 1) / ty);
@@ -895,6 +895,13 @@ int mhd_create(const mhd_grid* grid, double gamma, double cfl, const mhd_bc* bc,
         best_kz = kz;
       }
     }
+    // ... capped at 96 planes (measured, profiles/r02_ab_kz.txt): once the grid has several waves
+    // of CTAs, shorter chunks let the block scheduler even out the per-CTA time differences
+    // (edge tiles, ragged rows) and dispatch the short remainder chunk last, which the uniform
+    // model above does not see: 512^3 27.0 -> 25.8 ms per stage, 256^3 3.44 -> 3.39, 1024^3
+    // 203.9 -> 202.4 (kz 64-128 all within 1% of 96)
+    const long long kz_cap = 96;
+    if (best_kz > kz_cap) best_kz = kz_cap;
     const char* env = getenv("MHD_KZ");
     if (env && atoi(env) > 0) best_kz = atoi(env) < c->nzl ? atoi(env) : c->nzl;
     c->kz = (int)(best_kz > 0 ? best_kz : 1);
