@@ -275,7 +275,7 @@ def oracle_rate(ps, U, steps: int, warmup: int, threads: int = 0):
         oracle.set_num_threads(n0)
 
 
-def cpu_baseline(workload: str, p, scheme: str, steps: int = 6):
+def cpu_baseline(workload: str, p, scheme: str, steps: int = 12):
     """the oracle on all host cores (OMP_PROC_BIND=close, OMP_PLACES=cores) on
     a ~4 M-cell slab of the workload, `steps` steps, and on one core on a 1/8 slab; ~10-20 s"""
     model, sockets, cps, tpc = cpu_topology()
