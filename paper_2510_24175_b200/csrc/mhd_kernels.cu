@@ -222,6 +222,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
 #ifndef MHD_EDGE_HALO
 #define MHD_EDGE_HALO 1
 #endif
+#ifndef MHD_SKIP_RAGGED
+#define MHD_SKIP_RAGGED 1  // the ragged warps of the last tile row skip the faces no cell needs
+#endif
 constexpr int kEdgeHalo = MHD_EDGE_HALO;  // TMA window: halo slots converted per edge-warp thread
 #ifndef MHD_JOB_UNROLL
 #define MHD_JOB_UNROLL 1
@@ -540,13 +543,16 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
       // ---- select the face of this job (warp-uniform activity)
       int d = 0, row = ty, col = tx;
       bool active, cnt_right = false, cnt_face = false;
+      // (MHD_SKIP_RAGGED: a cell warp whose row lies beyond ny — the ragged last tile row — solves
+      // only the y face on the domain's top edge, the one face a valid cell needs)
+      const bool ragged = MHD_SKIP_RAGGED && cellw && gy >= ny;  // warp-uniform
       if (job == 0) {
-        active = DIM == 3 && cellw;
+        active = DIM == 3 && cellw && !ragged;
         d = 2;
         cnt_right = own && k + 1 < ke;
         cnt_face = own && (k + 1 < ke || a.zoff + k + 1 == a.nz_glob);
       } else if (job == 1) {
-        active = DIM >= 2 && full;
+        active = DIM >= 2 && full && !(ragged && gy > ny) && (cellw || !MHD_SKIP_RAGGED || y0 + TY <= ny);
         d = 1;
         if (cellw) {
           cnt_right = own;
@@ -562,10 +568,14 @@ __global__ void __launch_bounds__(32 * (TY + 1), (StageOcc<DIM, TY, REC>::value)
         col = TX;
         cnt_face = (x0 + TX == nx) && (y0 + tx < ny);
       } else {
-        active = cellw && full;
+        active = cellw && full && !ragged;
         d = 0;
         cnt_right = own;
         cnt_face = own || (gx == nx && gy < ny);
+        if (ragged && full) {  // (the x job's named barrier with the edge warp still needs this warp)
+          asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+          continue;
+        }
       }
       if (!active) continue;
       // ---- gather the two face states (normal frame)
